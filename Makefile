@@ -1,0 +1,34 @@
+# Top-level build: the product library (sm_100a CUDA + C ABI + C++ adapter)
+# and the oracle (test infrastructure).  `python -c "import __graft_entry__ as g; g.build()"`
+# runs the same recipe.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG := paper_2312_11918_b200
+LIB := $(PKG)/libfmha_b200.so
+SRCS := $(PKG)/csrc/fmha_api.cu $(PKG)/csrc/fmha_host.cpp
+HDRS := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp include/fmha/*.h include/fmha/*.hpp)
+
+all: $(LIB) oracle
+
+$(PKG)/csrc/tmem_ops.cuh: tools/gen_tmem_ops.py
+	python tools/gen_tmem_ops.py
+
+$(LIB): $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lpthread 2> build/ptxas.log || (cat build/ptxas.log; false)
+	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^/  /' || true
+
+oracle:
+	$(MAKE) -s -C oracle all
+
+build/ptxas.log: | build
+build:
+	mkdir -p build
+
+$(LIB): | build
+
+clean:
+	rm -f $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,195 @@
+"""paper_2312_11918_b200 -- B200-native (sm_100a) FMHA forward pass.
+
+Python mirror of the reference's pybind entry point
+``_fmhasim.fmha_forward(q, k, v, bM=64, bN=64, precision="f32")``
+(/root/reference/proj/src/bindings.cpp:81-91) on top of the C ABI in
+``include/fmha/fmha.h`` (loaded with ctypes from the in-tree
+``libfmha_b200.so``).  There is no CPU fallback: if the library or a GPU is
+missing, calls fail loudly.
+
+Three entry points:
+
+* :func:`fmha_forward` -- reference call shape: float32 numpy BSHD arrays in,
+  float32 out; ``precision`` is ``"f16emu"``/``"f16"`` or ``"bf16"``
+  (``"f32"`` raises ``ValueError``: the GPU path is 16-bit); invalid tiling
+  raises ``ValueError`` exactly like the reference (``test_smoke.py:43-46``).
+* :func:`fmha_fwd` -- device tensors (torch CUDA, fp16/bf16, BSHD with any
+  16-B aligned strides), asynchronous on the current stream, optional LSE.
+* :func:`fmha_fwd_host` -- host 16-bit buffers in/out (copies inside).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = ["lib", "fmha_forward", "fmha_fwd", "fmha_fwd_host", "attention_flops", "FmhaError",
+           "LIB_PATH", "F16", "BF16"]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfmha_b200.so")
+
+F16 = 0
+BF16 = 1
+OK, ERR_CONFIG, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 5, 6
+
+
+class FmhaError(RuntimeError):
+    """A CUDA-side failure of the FMHA library (status FMHA_ERR_CUDA)."""
+
+
+class FwdParams(C.Structure):
+    """fmha_fwd_params (include/fmha/fmha.h)."""
+    _fields_ = [("L", C.c_int64), ("N", C.c_int64), ("h", C.c_int64), ("d", C.c_int64),
+                ("q_stride", C.c_int64 * 3), ("k_stride", C.c_int64 * 3),
+                ("v_stride", C.c_int64 * 3), ("o_stride", C.c_int64 * 3),
+                ("scale", C.c_float), ("dtype", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the sm_100a library (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `make` or __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER(FwdParams)
+        vp = C.c_void_p
+        L.fmha_params_dense.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_float]
+        L.fmha_params_dense.restype = None
+        L.fmha_fwd_check.argtypes = [P]
+        L.fmha_fwd_check.restype = C.c_int
+        L.fmha_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp]
+        L.fmha_fwd.restype = C.c_int
+        L.fmha_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, C.c_int]
+        L.fmha_fwd_host.restype = C.c_int
+        L.fmha_forward_f32.argtypes = [vp, vp, vp] + [C.c_int64] * 6 + [C.c_int, C.c_float, vp, vp, C.c_int]
+        L.fmha_forward_f32.restype = C.c_int
+        L.fmha_attention_flops.argtypes = [C.c_int64] * 4
+        L.fmha_attention_flops.restype = C.c_int64
+        L.fmha_last_error.restype = C.c_char_p
+        L.fmha_last_launch_count.restype = C.c_int
+        L.fmha_version.restype = C.c_char_p
+        L.fmha_host_f32_to_16.argtypes = [C.c_float, C.c_int]
+        L.fmha_host_f32_to_16.restype = C.c_uint16
+        L.fmha_host_16_to_f32.argtypes = [C.c_uint16, C.c_int]
+        L.fmha_host_16_to_f32.restype = C.c_float
+        _lib = L
+    return _lib
+
+
+def _raise(status: int):
+    msg = lib().fmha_last_error().decode()
+    if status in (ERR_CONFIG, ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    raise FmhaError(f"fmha status {status}: {msg}")
+
+
+def _dtype_code(precision) -> int:
+    p = str(precision).lower().replace("torch.", "")
+    if p in ("f16", "f16emu", "fp16", "float16", "half"):
+        return F16
+    if p in ("bf16", "bfloat16"):
+        return BF16
+    if p in ("f32", "exactf32", "float32"):
+        raise ValueError("the GPU path is 16-bit: precision must be 'f16emu'/'f16' or 'bf16'")
+    raise ValueError("precision must be 'f16emu', 'f16' or 'bf16'")
+
+
+def attention_flops(L, N, h, d) -> int:
+    """4 * N^2 * d * h * L (attention_flops, attention.cpp:191-193)."""
+    return int(lib().fmha_attention_flops(L, N, h, d))
+
+
+def dense_params(L, N, h, d, dtype=F16, scale=0.0) -> FwdParams:
+    p = FwdParams()
+    lib().fmha_params_dense(C.byref(p), L, N, h, d, dtype, float(scale))
+    return p
+
+
+def fmha_forward(q, k, v, bM=64, bN=64, precision="f16emu", scale=None, return_lse=False, device=0):
+    """Reference call shape (bindings.cpp:81-91) on the GPU.
+
+    q, k, v: float32 arrays (L, N, h, d).  Inputs are rounded RNE to the
+    16-bit type (fp16 saturating like the reference's f16_round).  Returns
+    float32 O (and LSE (L, h, N) when ``return_lse``)."""
+    dt = _dtype_code(precision)
+    arrs = [np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v)]
+    for a in arrs:
+        if a.ndim != 4:
+            raise ValueError("expected a (L,N,h,d) array")
+    if not (arrs[0].shape == arrs[1].shape == arrs[2].shape):
+        raise ValueError("AttentionProblem: Q/K/V shape mismatch")
+    L, N, h, d = arrs[0].shape
+    o = np.empty((L, N, h, d), np.float32)
+    lse = np.empty((L, h, N), np.float32) if return_lse else None
+    st = lib().fmha_forward_f32(arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+                                L, N, h, d, bM, bN, dt, float(scale or 0.0), o.ctypes.data,
+                                lse.ctypes.data if lse is not None else None, device)
+    if st:
+        _raise(st)
+    return (o, lse) if return_lse else o
+
+
+def _strides(t, name):
+    s = t.stride()
+    if s[3] != 1:
+        raise ValueError(f"{name}: head-dim stride must be 1")
+    return (C.c_int64 * 3)(s[0], s[1], s[2])
+
+
+def fmha_fwd(q, k, v, o=None, lse=None, scale=None, stream=None, want_lse=True):
+    """Device entry point on torch CUDA tensors (L, N, h, d) fp16/bf16.
+
+    Returns (o, lse); allocates o / lse when not given.  Runs on ``stream``
+    (a torch.cuda.Stream) or the current stream."""
+    import torch
+
+    if q.dtype not in (torch.float16, torch.bfloat16):
+        raise ValueError("q/k/v must be float16 or bfloat16")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ValueError("q/k/v dtypes differ")
+    if not (q.shape == k.shape == v.shape) or q.dim() != 4:
+        raise ValueError("AttentionProblem: Q/K/V shape mismatch")
+    L, N, h, d = q.shape
+    if o is None:
+        o = torch.empty_like(q, memory_format=torch.contiguous_format)
+    if lse is None and want_lse:
+        lse = torch.empty((L, h, N), dtype=torch.float32, device=q.device)
+    p = FwdParams()
+    p.L, p.N, p.h, p.d = L, N, h, d
+    p.q_stride, p.k_stride, p.v_stride, p.o_stride = (_strides(q, "q"), _strides(k, "k"),
+                                                      _strides(v, "v"), _strides(o, "o"))
+    p.scale = float(scale or 0.0)
+    p.dtype = BF16 if q.dtype == torch.bfloat16 else F16
+    if stream is None:
+        stream = torch.cuda.current_stream(q.device)
+    st = lib().fmha_fwd(C.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                        lse.data_ptr() if lse is not None else None, stream.cuda_stream)
+    if st:
+        _raise(st)
+    return o, lse
+
+
+def fmha_fwd_host(q, k, v, o, lse=None, dtype=F16, scale=None, device=0):
+    """Host 16-bit buffers (numpy uint16 / float16 arrays, (L, N, h, d), dense):
+    H2D copies, kernel, D2H copies, synchronise.  Writes o (and lse)."""
+    L, N, h, d = q.shape
+    p = dense_params(L, N, h, d, dtype, scale or 0.0)
+    for a in (q, k, v, o):
+        if not a.flags["C_CONTIGUOUS"] or a.itemsize != 2:
+            raise ValueError("host buffers must be dense 16-bit arrays")
+    st = lib().fmha_fwd_host(C.byref(p), q.ctypes.data, k.ctypes.data, v.ctypes.data, o.ctypes.data,
+                             lse.ctypes.data if lse is not None else None, device)
+    if st:
+        _raise(st)
+    return o, lse
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the last fmha_fwd call on this thread."""
+    return int(lib().fmha_last_launch_count())

@@ -1,0 +1,349 @@
+// fmha_fwd_kernel.cuh -- warp-specialised FMHA forward for sm_100a, head
+// dim 64 / 128.
+//
+// Replaces the arithmetic of fmhasim::fmha_forward
+// (/root/reference/proj/src/attention.cpp:153-173): for every (b, head) and
+// every 128-row Q tile it streams 128-row K/V tiles (the reference's KBLK),
+// computes S = Q K^T (GEMM-I, attention.cpp:123), the online softmax update
+// (online_softmax_step, attention.cpp:36-66), O += P V (GEMM-II,
+// attention.cpp:130) and the final O *= 1/Sigma (rowwise_finalize,
+// attention.cpp:68-73), plus LSE = m + ln(Sigma).
+//
+// CTA = one (b, head) and TWO 128-row Q tiles (256 query rows) that share
+// every K/V tile loaded into shared memory.
+//
+//   warps 0-3  softmax WG 0: thread t owns row t of Q tile 0 (TMEM lane t)
+//   warps 4-7  softmax WG 1: same for Q tile 1
+//   warp 8     TMA producer (one elected lane): Q0, Q1, then K0 V0 K1 V1 ...
+//   warp 9     MMA issuer (one lane) + TMEM allocator
+//
+// Tensor Memory (512 columns x 128 lanes x 32 bit):
+//   S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D,256+2D)
+//   P_q (16-bit, packed 2 per column) aliases the first 64 columns of S_q.
+//
+// Per K/V tile j the MMA warp issues, in order,
+//   PV0(j-1) ; S0(j) ; PV1(j-1) ; S1(j)
+// so the tensor core runs tile 1's GEMMs while softmax WG 0 works on S0(j)
+// and vice versa (two-tile ping-pong).  tcgen05 ops from one thread execute
+// in issue order, so when softmax WG q observes "S_q(j) complete" the
+// preceding PV_q(j-1) has completed too: the WG may rescale O_q in TMEM
+// without any further barrier, and P_q(j) may overwrite S_q(j)'s columns.
+//
+// Rescaling is conditional (FlashAttention-4 style): a warp keeps its stale
+// row max unless some row's max grew by more than 2^8 in the exp2 domain.
+// Exact, because the final (m, Sigma) pair is consistent; P stays <= 256.
+#pragma once
+
+#include <cuda.h>
+#include <cstdint>
+
+#include "sm100.cuh"
+#include "tmem_ops.cuh"
+
+namespace fmha_b200 {
+
+struct FwdArgs {
+  void* o;                   // BSHD output, 16-bit
+  float* lse;                // [L][h][N] fp32 or nullptr
+  int64_t o_sb, o_sn, o_sh;  // output strides (elements)
+  int N, H;
+  int n_kv_tiles;    // ceil(N / 128)
+  float scale_log2;  // softmax scale * log2(e)
+  float scale;       // softmax scale (natural)
+};
+
+template <int D>
+struct FwdCfg {
+  static_assert(D == 64 || D == 128, "this kernel handles head dim 64 and 128");
+  static constexpr int kBM = 128;         // Q rows per tile (UMMA M)
+  static constexpr int kBN = 128;         // K/V rows per tile
+  static constexpr int kChunks = D / 64;  // 128-B swizzle atoms along d
+  static constexpr int kQTileBytes = kBM * D * 2;
+  static constexpr int kKVTileBytes = kBN * D * 2;
+  static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
+  static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kSmemRing = kStages * kKVTileBytes;
+  static constexpr int kNumBars = 1 + 2 * kStages + 6;
+  static constexpr int kSmemBytes = kSmemQ + kSmemRing + kNumBars * 8 + 16;
+  static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
+  static constexpr int kThreads = 320;
+  static constexpr int kLoadWarp = 8;
+  static constexpr int kMmaWarp = 9;
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
+  static constexpr uint32_t kTmemCols = 512;
+};
+
+template <int D, bool kBF16>
+__global__ void __launch_bounds__(320, 1)
+    fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+  using C = FwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B alignment for the 128-B swizzle atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sRing = smem + C::kSmemQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing);
+  uint64_t* bar_q = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;  // [2]
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_full = p_full + 2;             // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int b = blockIdx.z;
+  const int qrow0 = blockIdx.x * 2 * C::kBM;
+  const int n_kv = args.n_kv_tiles;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&s_full[q], 1);
+      mbar_init(&p_full[q], 128);
+      mbar_init(&o_full[q], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == C::kLoadWarp) {
+    // ---------------------------------------------------- TMA producer --
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      const uint64_t keep = l2_policy_evict_last();   // K/V re-read by sibling CTAs
+      const uint64_t once = l2_policy_evict_first();  // Q read once
+      mbar_arrive_expect_tx(bar_q, 2 * C::kQTileBytes);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_4d_hint(&tmQ, bar_q, sQ + q * C::kQTileBytes + c * C::kBM * 128, c * 64, head,
+                           qrow0 + q * C::kBM, b, once);
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_kv; ++j) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&kv_empty[slot], phase ^ 1);
+          mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
+          uint8_t* dst = sRing + slot * C::kKVTileBytes;
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_4d_hint(t == 0 ? &tmK : &tmV, &kv_full[slot], dst + c * C::kBN * 128, c * 64,
+                             head, j * C::kBN, b, keep);
+          if (++slot == C::kStages) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ------------------------------------------------------ MMA issuer --
+    if (lane == 0) {
+      constexpr uint32_t kIdescQK = idesc_f16(kBF16, C::kBM, C::kBN, false, false);
+      constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
+      const uint32_t sQ_addr = smem_u32(sQ);
+      const uint32_t ring_addr = smem_u32(sRing);
+      int slot = 0;
+      uint32_t phase = 0;
+      auto next_slot = [&]() -> int {
+        const int s = slot;
+        mbar_wait(&kv_full[s], phase);
+        if (++slot == C::kStages) {
+          slot = 0;
+          phase ^= 1;
+        }
+        return s;
+      };
+      // S_q = Q_q K^T : M=128, N=128, K=D in D/16 steps of 32 B inside the
+      // 128-B swizzle atom; the next 64 columns of d live in the next atom
+      // column (chunk stride = rows * 128 B).
+      auto mma_qk = [&](int q, int kslot) {
+        const uint32_t a0 = sQ_addr + q * C::kQTileBytes;
+        const uint32_t b0 = ring_addr + kslot * C::kKVTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
+          const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
+          mma_ss(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0 + off_a, 16, 1024),
+                 sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+        }
+      };
+      // O_q (+)= P_q V : M=128, N=D, K=128 kv rows in 8 steps of 16 rows.
+      // A = P from TMEM (8 columns per step); B = V, MN-major (d contiguous):
+      // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.
+      auto mma_pv = [&](int q, int vslot, bool accumulate) {
+        const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
+        const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
+#pragma unroll
+        for (int kk = 0; kk < C::kBN / 16; ++kk) {
+          mma_ts(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
+                 sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
+                 (accumulate || kk > 0) ? 1u : 0u);
+        }
+      };
+
+      mbar_wait(bar_q, 0);
+      int ks = next_slot();
+      tc_fence_after();
+      mma_qk(0, ks);
+      mma_commit(&s_full[0]);
+      mma_qk(1, ks);
+      mma_commit(&s_full[1]);
+      mma_commit(&kv_empty[ks]);
+      for (int j = 1; j < n_kv; ++j) {
+        const int vs = next_slot();
+        ks = next_slot();
+        const uint32_t par = (j - 1) & 1;
+        mbar_wait(&p_full[0], par);
+        tc_fence_after();
+        mma_pv(0, vs, j > 1);
+        mma_qk(0, ks);
+        mma_commit(&s_full[0]);
+        mbar_wait(&p_full[1], par);
+        tc_fence_after();
+        mma_pv(1, vs, j > 1);
+        mma_qk(1, ks);
+        mma_commit(&s_full[1]);
+        mma_commit(&kv_empty[vs]);
+        mma_commit(&kv_empty[ks]);
+      }
+      const int vs = next_slot();
+      const uint32_t par = (n_kv - 1) & 1;
+      mbar_wait(&p_full[0], par);
+      tc_fence_after();
+      mma_pv(0, vs, n_kv > 1);
+      mma_commit(&o_full[0]);
+      mbar_wait(&p_full[1], par);
+      tc_fence_after();
+      mma_pv(1, vs, n_kv > 1);
+      mma_commit(&o_full[1]);
+      mma_commit(&kv_empty[vs]);
+    }
+  } else {
+    // ------------------------------------------------- softmax WG 0 / 1 --
+    const int q = warp >> 2;
+    const int r = threadIdx.x & 127;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + (q ? C::kColS1 : C::kColS0);
+    const uint32_t tO = tmem + lane_off + (q ? C::kColO1 : C::kColO0);
+    const float sl2 = args.scale_log2;
+    const int N = args.N;
+    float m = -INFINITY;  // running max in raw score units
+    float l = 0.0f;       // running sum of exp2((s - m) * sl2)
+
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&s_full[q], j & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+      tmem_ld32x32b_x128(tS, sr);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
+      const int valid = N - j * C::kBN;  // columns >= valid are padding
+      if (valid < C::kBN) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) s[c] = -INFINITY;
+      }
+      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+      for (int c = 4; c < 128; c += 4) {
+        mx0 = fmaxf(mx0, s[c]);
+        mx1 = fmaxf(mx1, s[c + 1]);
+        mx2 = fmaxf(mx2, s[c + 2]);
+        mx3 = fmaxf(mx3, s[c + 3]);
+      }
+      const float m_new = fmaxf(m, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
+      const bool need = (m_new - m) * sl2 > 8.0f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = ex2_approx((m - m_new) * sl2);
+        l *= alpha;
+        if (j > 0) {
+          // O_q(j-1) is complete (see header); rescale this lane's row
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32x32b_x32(tO + c * 32, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32x32b_x32(tO + c * 32, o);
+          }
+        }
+        m = m_new;
+      }
+      const float neg = -m * sl2;
+      float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
+      uint32_t p[64];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const float e0 = ex2_approx(fmaf(s[2 * i], sl2, neg));
+        const float e1 = ex2_approx(fmaf(s[2 * i + 1], sl2, neg));
+        const float e2 = ex2_approx(fmaf(s[2 * i + 2], sl2, neg));
+        const float e3 = ex2_approx(fmaf(s[2 * i + 3], sl2, neg));
+        rs0 += e0;
+        rs1 += e1;
+        rs2 += e2;
+        rs3 += e3;
+        p[i] = pack2<kBF16>(e0, e1);
+        p[i + 1] = pack2<kBF16>(e2, e3);
+      }
+      tmem_st32x32b_x64(tS, p);
+      l += (rs0 + rs1) + (rs2 + rs3);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[q]);
+    }
+
+    // ------------------------------------------------------- epilogue --
+    mbar_wait(&o_full[q], 0);
+    tc_fence_after();
+    const int row = qrow0 + q * C::kBM + r;
+    const bool row_ok = row < N;
+    const float inv = 1.0f / l;
+    uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
+                     static_cast<int64_t>(row_ok ? row : 0) * args.o_sn +
+                     static_cast<int64_t>(head) * args.o_sh;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32x32b_x32(tO + c * 32, o);  // warp-collective: every lane loads
+      uint32_t h2[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        h2[i] = pack2<kBF16>(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+      if (row_ok) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          st_global_v4(orow + c * 32 + v * 8, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2],
+                       h2[4 * v + 3]);
+      }
+    }
+    if (row_ok && args.lse != nullptr)
+      args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == C::kMmaWarp) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+}  // namespace fmha_b200
