@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -75,11 +76,29 @@ float resolve_scale(const fmha_fwd_params* p) {
   return p->scale > 0.0f ? p->scale : static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->d)));
 }
 
-template <int D, bool BF16>
+// Debug timeline buffer (FMHA_TRACE=1): see FwdArgs::trace.
+unsigned long long* trace_buffer(size_t n) {
+  static unsigned long long* buf = nullptr;
+  static size_t cap = 0;
+  static const bool on = [] {
+    const char* e = std::getenv("FMHA_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return nullptr;
+  if (cap < n) {
+    if (buf) cudaFree(buf);
+    if (cudaMalloc(&buf, n * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(buf, 0, n * sizeof(unsigned long long));
+    cap = n;
+  }
+  return buf;
+}
+
+template <int D, bool BF16, int EMU = 0>
 fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
   using Cfg = fmha_b200::FwdCfg<D>;
-  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16>;
+  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -98,6 +117,7 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = trace_buffer(static_cast<size_t>(2 * a.n_kv_tiles * 8));
   dim3 grid(static_cast<unsigned>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM)),
             static_cast<unsigned>(p->h), static_cast<unsigned>(p->L));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
@@ -130,6 +150,7 @@ fmha_status launch_d256(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = nullptr;
   dim3 grid(static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
             static_cast<unsigned>(p->L));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
@@ -154,6 +175,13 @@ Workspace& workspace(int device) {
 }  // namespace
 
 extern "C" {
+
+// Debug only: copy the FMHA_TRACE timeline (n entries) to host memory.
+int fmha_debug_trace_copy(unsigned long long* host, int64_t n) {
+  unsigned long long* b = trace_buffer(static_cast<size_t>(n));
+  if (!b) return -1;
+  return cudaMemcpy(host, b, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
 
 const char* fmha_version(void) { return "paper_2312_11918_b200 0.1.0 (sm_100a)"; }
 
@@ -219,9 +247,27 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     case 64:
       return bf ? launch_d128<64, true>(p, mq, mk, mv, o, lse, st)
                 : launch_d128<64, false>(p, mq, mk, mv, o, lse, st);
-    case 128:
-      return bf ? launch_d128<128, true>(p, mq, mk, mv, o, lse, st)
-                : launch_d128<128, false>(p, mq, mk, mv, o, lse, st);
+    case 128: {
+      // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default: all MUFU)
+      static const int emu = [] {
+        const char* e = std::getenv("FMHA_TUNE_EMU");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (emu == 0)
+        return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, o, lse, st)
+                  : launch_d128<128, false, 0>(p, mq, mk, mv, o, lse, st);
+      if (emu == 4)
+        return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, o, lse, st)
+                  : launch_d128<128, false, 4>(p, mq, mk, mv, o, lse, st);
+      if (emu == 8)
+        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, o, lse, st)
+                  : launch_d128<128, false, 8>(p, mq, mk, mv, o, lse, st);
+      if (emu == 6)
+        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, o, lse, st)
+                  : launch_d128<128, false, 6>(p, mq, mk, mv, o, lse, st);
+      return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, o, lse, st)
+                : launch_d128<128, false, 0>(p, mq, mk, mv, o, lse, st);
+    }
     default:
       return bf ? launch_d256<true>(p, mq, mk, mv, o, lse, st)
                 : launch_d256<false>(p, mq, mk, mv, o, lse, st);

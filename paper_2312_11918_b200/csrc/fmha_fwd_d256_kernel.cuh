@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == C::kMmaWarp) {
-    if (lane == 0) {
+    {  // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t kIdescQK = idesc_f16(kBF16, C::kBM, C::kBN, false, false);
       constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
       const uint32_t sQ_addr = smem_u32(sQ);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
           const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
-          mma_ss(tmem + C::col_s(buf), sdesc_sw128(sQ_addr + off_a, 16, 1024),
+          mma_ss_elect(tmem + C::col_s(buf), sdesc_sw128(sQ_addr + off_a, 16, 1024),
                  sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
 #pragma unroll
         for (int kk = 0; kk < C::kBN / 16; ++kk)
-          mma_ts(tmem + C::kColO, tmem + C::col_s(buf) + kk * 8,
+          mma_ts_elect(tmem + C::kColO, tmem + C::col_s(buf) + kk * 8,
                  sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
                  (accumulate || kk > 0) ? 1u : 0u);
       };
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(192, 1)
         const int ks = wait_item(2 * t);
         tc_fence_after();
         mma_qk(t, ks);
-        mma_commit(&s_full[t]);
-        mma_commit(&kv_empty[ks]);
+        mma_commit_elect(&s_full[t]);
+        mma_commit_elect(&kv_empty[ks]);
       }
       for (int j = 0; j < n_kv; ++j) {
         const int buf = j & 1;
@@ -164,17 +164,17 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&p_full[buf], static_cast<uint32_t>(j >> 1) & 1);
         tc_fence_after();
         mma_pv(buf, vs, j > 0);
-        mma_commit(pv_done);
-        mma_commit(&kv_empty[vs]);
+        mma_commit_elect(pv_done);
+        mma_commit_elect(&kv_empty[vs]);
         if (j + 2 < n_kv) {
           const int ks = wait_item(2 * (j + 2));
           tc_fence_after();
           mma_qk(buf, ks);
-          mma_commit(&s_full[buf]);
-          mma_commit(&kv_empty[ks]);
+          mma_commit_elect(&s_full[buf]);
+          mma_commit_elect(&kv_empty[ks]);
         }
       }
-      mma_commit(o_full);
+      mma_commit_elect(o_full);
     }
   } else {
     const int r = threadIdx.x & 127;

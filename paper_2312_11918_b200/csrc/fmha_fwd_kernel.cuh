@@ -38,6 +38,7 @@
 #include <cstdint>
 
 #include "sm100.cuh"
+#include "softmax_math.cuh"
 #include "tmem_ops.cuh"
 
 namespace fmha_b200 {
@@ -50,7 +51,16 @@ struct FwdArgs {
   int n_kv_tiles;    // ceil(N / 128)
   float scale_log2;  // softmax scale * log2(e)
   float scale;       // softmax scale (natural)
+  unsigned long long* trace;  // debug timeline (FMHA_TRACE=1) or nullptr
 };
+
+// Debug timeline for CTA (0,0,0): clock64 stamps written by one thread per
+// role.  trace[(q * n_kv + j) * 8 + k]:
+//   k=0 softmax woke (S ready)  1 S in registers  2 row max done
+//   3 P stored + arrived        4 MMA saw P ready  5 MMA issued PV+S
+__device__ __forceinline__ void trace_stamp(const FwdArgs& a, bool on, int q, int j, int k) {
+  if (on) a.trace[(q * a.n_kv_tiles + j) * 8 + k] = clock64();
+}
 
 template <int D>
 struct FwdCfg {
@@ -66,15 +76,16 @@ struct FwdCfg {
   static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kSmemBytes = kSmemQ + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
-  static constexpr int kThreads = 320;
+  static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
   static constexpr int kLoadWarp = 8;
   static constexpr int kMmaWarp = 9;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
 };
 
-template <int D, bool kBF16>
-__global__ void __launch_bounds__(320, 1)
+// kEmuPer16: of every 16 score pairs, how many take the FMA-pipe exp2.
+template <int D, bool kBF16, int kEmuPer16 = 0>
+__global__ void __launch_bounds__(384, 1)
     fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
@@ -100,6 +111,7 @@ __global__ void __launch_bounds__(320, 1)
   const int b = blockIdx.z;
   const int qrow0 = blockIdx.x * 2 * C::kBM;
   const int n_kv = args.n_kv_tiles;
+  const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
@@ -120,6 +132,11 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
+  // Register split (setmaxnreg inside each role's branch so ptxas sees one
+  // limit per region): the load/MMA warpgroup needs few registers, the
+  // softmax warpgroups hold a 128-column S row plus packed P per thread.
+  if (warp >= 8) {
+    reg_dealloc<112>();
   if (warp == C::kLoadWarp) {
     // ---------------------------------------------------- TMA producer --
     if (lane == 0) {
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------------ MMA issuer --
-    if (lane == 0) {
+    {  // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t kIdescQK = idesc_f16(kBF16, C::kBM, C::kBN, false, false);
       constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
       const uint32_t sQ_addr = smem_u32(sQ);
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
           const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
-          mma_ss(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0 + off_a, 16, 1024),
+          mma_ss_elect(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0 + off_a, 16, 1024),
                  sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
 #pragma unroll
         for (int kk = 0; kk < C::kBN / 16; ++kk) {
-          mma_ts(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
+          mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
                  sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
                  (accumulate || kk > 0) ? 1u : 0u);
         }
@@ -204,40 +221,46 @@ __global__ void __launch_bounds__(320, 1)
       int ks = next_slot();
       tc_fence_after();
       mma_qk(0, ks);
-      mma_commit(&s_full[0]);
+      mma_commit_elect(&s_full[0]);
       mma_qk(1, ks);
-      mma_commit(&s_full[1]);
-      mma_commit(&kv_empty[ks]);
+      mma_commit_elect(&s_full[1]);
+      mma_commit_elect(&kv_empty[ks]);
       for (int j = 1; j < n_kv; ++j) {
         const int vs = next_slot();
         ks = next_slot();
         const uint32_t par = (j - 1) & 1;
         mbar_wait(&p_full[0], par);
+        trace_stamp(args, tr, 0, j - 1, 4);
         tc_fence_after();
         mma_pv(0, vs, j > 1);
         mma_qk(0, ks);
-        mma_commit(&s_full[0]);
+        mma_commit_elect(&s_full[0]);
+        trace_stamp(args, tr, 0, j - 1, 5);
         mbar_wait(&p_full[1], par);
+        trace_stamp(args, tr, 1, j - 1, 4);
         tc_fence_after();
         mma_pv(1, vs, j > 1);
         mma_qk(1, ks);
-        mma_commit(&s_full[1]);
-        mma_commit(&kv_empty[vs]);
-        mma_commit(&kv_empty[ks]);
+        mma_commit_elect(&s_full[1]);
+        trace_stamp(args, tr, 1, j - 1, 5);
+        mma_commit_elect(&kv_empty[vs]);
+        mma_commit_elect(&kv_empty[ks]);
       }
       const int vs = next_slot();
       const uint32_t par = (n_kv - 1) & 1;
       mbar_wait(&p_full[0], par);
       tc_fence_after();
       mma_pv(0, vs, n_kv > 1);
-      mma_commit(&o_full[0]);
+      mma_commit_elect(&o_full[0]);
       mbar_wait(&p_full[1], par);
       tc_fence_after();
       mma_pv(1, vs, n_kv > 1);
-      mma_commit(&o_full[1]);
-      mma_commit(&kv_empty[vs]);
+      mma_commit_elect(&o_full[1]);
+      mma_commit_elect(&kv_empty[vs]);
     }
+  }
   } else {
+    reg_alloc<192>();
     // ------------------------------------------------- softmax WG 0 / 1 --
     const int q = warp >> 2;
     const int r = threadIdx.x & 127;
@@ -251,9 +274,12 @@ __global__ void __launch_bounds__(320, 1)
 
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[q], j & 1);
+      const bool trr = tr && r == 0;
+      trace_stamp(args, trr, q, j, 0);
       tc_fence_after();
       uint32_t sr[128];
       tmem_ld32x32b_x128(tS, sr);
+      trace_stamp(args, trr, q, j, 1);
       float s[128];
 #pragma unroll
       for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
@@ -272,6 +298,7 @@ __global__ void __launch_bounds__(320, 1)
         mx3 = fmaxf(mx3, s[c + 3]);
       }
       const float m_new = fmaxf(m, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
+      trace_stamp(args, trr, q, j, 2);
       const bool need = (m_new - m) * sl2 > 8.0f;
       if (__any_sync(0xffffffffu, need)) {
         const float alpha = ex2_approx((m - m_new) * sl2);
@@ -290,26 +317,26 @@ __global__ void __launch_bounds__(320, 1)
         m = m_new;
       }
       const float neg = -m * sl2;
-      float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
-      uint32_t p[64];
-#pragma unroll
-      for (int i = 0; i < 64; i += 2) {
-        const float e0 = ex2_approx(fmaf(s[2 * i], sl2, neg));
-        const float e1 = ex2_approx(fmaf(s[2 * i + 1], sl2, neg));
-        const float e2 = ex2_approx(fmaf(s[2 * i + 2], sl2, neg));
-        const float e3 = ex2_approx(fmaf(s[2 * i + 3], sl2, neg));
-        rs0 += e0;
-        rs1 += e1;
-        rs2 += e2;
-        rs3 += e3;
-        p[i] = pack2<kBF16>(e0, e1);
-        p[i + 1] = pack2<kBF16>(e2, e3);
+      // exponentiate and store P in two 64-column halves (32 packed columns
+      // each) so only half of P is live in registers at a time
+      float rowsum;
+      {
+        uint32_t p[32];
+        rowsum = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
+                                : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
+        tmem_st32x32b_x32(tS, p);
       }
-      tmem_st32x32b_x64(tS, p);
-      l += (rs0 + rs1) + (rs2 + rs3);
+      {
+        uint32_t p[32];
+        rowsum += valid < C::kBN ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p)
+                                 : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p);
+        tmem_st32x32b_x32(tS + 32, p);
+      }
+      l += rowsum;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[q]);
+      trace_stamp(args, trr, q, j, 3);
     }
 
     // ------------------------------------------------------- epilogue --

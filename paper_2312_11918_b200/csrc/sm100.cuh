@@ -52,9 +52,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// Wait for the phase with the given parity to complete.  With FMHA_WATCHDOG
-// (default on) a wait longer than ~4 s traps instead of hanging the GPU: a
-// protocol bug then surfaces as a launch error, not a dead box.
+// Wait for the phase with the given parity to complete.  The watchdog
+// (default on; -DFMHA_NO_WATCHDOG removes it) traps after ~4 s instead of
+// hanging the GPU, so a protocol bug surfaces as a launch error, not a dead
+// box.  -DFMHA_WATCHDOG_PRINTF adds a diagnostic line (costs registers).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
@@ -62,8 +63,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) {
+#ifdef FMHA_WATCHDOG_PRINTF
       printf("fmha watchdog: block (%d,%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n",
              blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, a, parity);
+#endif
       __trap();
     }
   }
@@ -198,6 +201,39 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Warp-collective variants: the whole warp executes them with warp-uniform
+// operands and one lane (elect.sync) issues.  Keeping the MMA warp converged
+// lets ptxas hold descriptors in uniform registers instead of a per-lane
+// waterfall loop around every UTCHMMA.
+__device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
       : "memory");
 }
 

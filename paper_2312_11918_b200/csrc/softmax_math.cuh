@@ -1,0 +1,120 @@
+// softmax_math.cuh -- the per-row math of online_softmax_step
+// (/root/reference/proj/src/attention.cpp:36-66) tuned for sm_100a:
+//
+//  * packed fp32x2 FMA / ADD (FFMA2 / FADD2) for x = s*c - m*c and the row sum;
+//  * exp2 split between the MUFU unit (ex2.approx) and a degree-4 polynomial
+//    on the FMA pipe (Cody-Waite split x = n + f, f in [-1/2, 1/2], 2^f by a
+//    minimax polynomial, 2^n added into the exponent field).  At d <= 128 the
+//    MUFU ex2 rate (16/clk/SM) otherwise equals the tensor-core rate per score
+//    (SURVEY.md 7.2), so moving ~40% of the exponentials to the FMA pipe is
+//    what lets the tensor core, not the exponential, set the pace;
+//  * P packed to 16-bit pairs for the TMEM store (cvt.rn.{f16,bf16}x2).
+//
+// Polynomial max relative error 2.6e-6 (well below fp16 / bf16 rounding of
+// P); inputs are clamped at -125 so fully masked scores give ~2e-38, which
+// rounds to 0 in fp16 and contributes < 1e-37 in bf16.
+#pragma once
+
+#include <cstdint>
+
+#include "sm100.cuh"
+
+namespace fmha_b200 {
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair, on the FMA + ALU pipes only.
+__device__ __forceinline__ uint64_t exp2_poly_x2(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  x = f2_pack(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+  const uint64_t kMagic = f2_pack(12582912.0f, 12582912.0f);  // 1.5 * 2^23: round to integer
+  const uint64_t kNegMagic = f2_pack(-12582912.0f, -12582912.0f);
+  const uint64_t kMinus1 = f2_pack(-1.0f, -1.0f);
+  const uint64_t t = fadd2(x, kMagic);          // low mantissa bits hold n = rint(x)
+  const uint64_t n = fadd2(t, kNegMagic);       // n as float
+  const uint64_t f = ffma2(n, kMinus1, x);      // f = x - n in [-0.5, 0.5]
+  uint64_t p = ffma2(f2_pack(0.00957564264535904f, 0.00957564264535904f), f,
+                     f2_pack(0.05591900646686554f, 0.05591900646686554f));
+  p = ffma2(p, f, f2_pack(0.24024616181850433f, 0.24024616181850433f));
+  p = ffma2(p, f, f2_pack(0.693121612071991f, 0.693121612071991f));
+  p = ffma2(p, f, f2_pack(0.9999992847442627f, 0.9999992847442627f));
+  float t0, t1, p0, p1;
+  f2_unpack(t, t0, t1);
+  f2_unpack(p, p0, p1);
+  // (t_bits << 23) == n << 23 for |n| < 256; add it into the exponent field
+  const uint32_t r0 = __float_as_uint(p0) + (__float_as_uint(t0) << 23);
+  const uint32_t r1 = __float_as_uint(p1) + (__float_as_uint(t1) << 23);
+  return f2_pack(__uint_as_float(r0), __uint_as_float(r1));
+}
+
+__device__ __forceinline__ uint64_t exp2_mufu_x2(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  return f2_pack(ex2_approx(x0), ex2_approx(x1));
+}
+
+template <bool kBF16>
+__device__ __forceinline__ uint32_t pack2_x2(uint64_t e) {
+  float lo, hi;
+  f2_unpack(e, lo, hi);
+  return pack2<kBF16>(lo, hi);
+}
+
+// P = 2^(s*c - m*c) for the kCols scores s[kOff .. kOff+kCols) of one row;
+// returns the fp32 sum of the UNROUNDED P (attention.cpp:50-55) and writes
+// the 16-bit packed P.  Pairs with (i % 16) < kEmuPer16 use the polynomial.
+template <bool kBF16, int kOff, int kCols, int kEmuPer16, int kTotal>
+__device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float c, float neg_mc,
+                                                 uint32_t (&p)[kCols / 2]) {
+  const uint64_t c2 = f2_pack(c, c);
+  const uint64_t nm2 = f2_pack(neg_mc, neg_mc);
+  uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = f2_pack(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < kCols / 2; ++i) {
+    const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
+    const uint64_t e = ((i & 15) < kEmuPer16) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    if (i & 1)
+      acc1 = fadd2(acc1, e);
+    else
+      acc0 = fadd2(acc0, e);
+    p[i] = pack2_x2<kBF16>(e);
+  }
+  float a0, a1, b0, b1;
+  f2_unpack(acc0, a0, a1);
+  f2_unpack(acc1, b0, b1);
+  return (a0 + b0) + (a1 + b1);
+}
+
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegs));
+}
+
+}  // namespace fmha_b200
