@@ -18,6 +18,11 @@ $(LIB): $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lpthread 2> build/ptxas.log || (cat build/ptxas.log; false)
 	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^/  /' || true
 
+# timeline-instrumented build for tools/trace_timeline.py (FMHA_B200_LIB selects it)
+trace: build/libfmha_b200_trace.so
+build/libfmha_b200_trace.so: $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh | build
+	$(NVCC) $(NVFLAGS) -DFMHA_TRACE_BUILD -shared -o $@ $(SRCS) -lpthread 2> build/ptxas_trace.log || (cat build/ptxas_trace.log; false)
+
 oracle:
 	$(MAKE) -s -C oracle all
 
@@ -31,4 +36,4 @@ clean:
 	rm -f $(LIB)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean trace

@@ -28,7 +28,8 @@ __all__ = ["lib", "fmha_forward", "fmha_fwd", "fmha_fwd_host", "attention_flops"
            "LIB_PATH", "F16", "BF16"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfmha_b200.so")
+# FMHA_B200_LIB selects an alternative build (e.g. build/libfmha_b200_trace.so)
+LIB_PATH = os.environ.get("FMHA_B200_LIB") or os.path.join(HERE, "libfmha_b200.so")
 
 F16 = 0
 BF16 = 1

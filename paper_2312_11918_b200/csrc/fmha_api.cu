@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -94,9 +95,18 @@ unsigned long long* trace_buffer(size_t n) {
   return buf;
 }
 
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 template <int D, bool BF16, int EMU = 0>
 fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
-                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+                        const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st) {
   using Cfg = fmha_b200::FwdCfg<D>;
   auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
   static bool attr_set = false;  // benign race: idempotent attribute set
@@ -106,21 +116,19 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     attr_set = true;
   }
-  fmha_b200::FwdArgs a;
-  a.o = o;
+  fmha_b200::FwdArgs a{};
   a.lse = lse;
-  a.o_sb = p->o_stride[0];
-  a.o_sn = p->o_stride[1];
-  a.o_sh = p->o_stride[2];
   a.N = static_cast<int>(p->N);
   a.H = static_cast<int>(p->h);
+  a.L = static_cast<int>(p->L);
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
+  a.n_qblocks = static_cast<int>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
+  a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
   a.trace = trace_buffer(static_cast<size_t>(2 * a.n_kv_tiles * 8));
-  dim3 grid(static_cast<unsigned>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM)),
-            static_cast<unsigned>(p->h), static_cast<unsigned>(p->L));
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
+  const int grid = std::min(a.n_units, num_sms());
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   g_last_launches = 1;
@@ -139,7 +147,7 @@ fmha_status launch_d256(const fmha_fwd_params* p, const CUtensorMap& mq, const C
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     attr_set = true;
   }
-  fmha_b200::FwdArgs a;
+  fmha_b200::FwdArgs a{};
   a.o = o;
   a.lse = lse;
   a.o_sb = p->o_stride[0];
@@ -236,17 +244,18 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     return fail(FMHA_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
   const int rows = 128;
   const int kv_rows = p->d == 256 ? 64 : 128;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, p->dtype, p, p->q_stride, rows) ||
       !make_map(&mk, k, p->dtype, p, p->k_stride, kv_rows) ||
-      !make_map(&mv, v, p->dtype, p, p->v_stride, kv_rows))
+      !make_map(&mv, v, p->dtype, p, p->v_stride, kv_rows) ||
+      !make_map(&mo, o, p->dtype, p, p->o_stride, rows))
     return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or arguments)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool bf = p->dtype == FMHA_BF16;
   switch (p->d) {
     case 64:
-      return bf ? launch_d128<64, true>(p, mq, mk, mv, o, lse, st)
-                : launch_d128<64, false>(p, mq, mk, mv, o, lse, st);
+      return bf ? launch_d128<64, true>(p, mq, mk, mv, mo, lse, st)
+                : launch_d128<64, false>(p, mq, mk, mv, mo, lse, st);
     case 128: {
       // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default: all MUFU)
       static const int emu = [] {
@@ -254,19 +263,19 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
         return e ? std::atoi(e) : 0;
       }();
       if (emu == 0)
-        return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, o, lse, st)
-                  : launch_d128<128, false, 0>(p, mq, mk, mv, o, lse, st);
+        return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
       if (emu == 4)
-        return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, o, lse, st)
-                  : launch_d128<128, false, 4>(p, mq, mk, mv, o, lse, st);
+        return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
       if (emu == 8)
-        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, o, lse, st)
-                  : launch_d128<128, false, 8>(p, mq, mk, mv, o, lse, st);
+        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st);
       if (emu == 6)
-        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, o, lse, st)
-                  : launch_d128<128, false, 6>(p, mq, mk, mv, o, lse, st);
-      return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, o, lse, st)
-                : launch_d128<128, false, 0>(p, mq, mk, mv, o, lse, st);
+        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st);
+      return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
+                : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
     }
     default:
       return bf ? launch_d256<true>(p, mq, mk, mv, o, lse, st)

@@ -1,5 +1,5 @@
-// fmha_fwd_kernel.cuh -- warp-specialised FMHA forward for sm_100a, head
-// dim 64 / 128.
+// fmha_fwd_kernel.cuh -- persistent, warp-specialised FMHA forward for
+// sm_100a, head dim 64 / 128.
 //
 // Replaces the arithmetic of fmhasim::fmha_forward
 // (/root/reference/proj/src/attention.cpp:153-173): for every (b, head) and
@@ -9,13 +9,18 @@
 // attention.cpp:130) and the final O *= 1/Sigma (rowwise_finalize,
 // attention.cpp:68-73), plus LSE = m + ln(Sigma).
 //
-// CTA = one (b, head) and TWO 128-row Q tiles (256 query rows) that share
-// every K/V tile loaded into shared memory.
+// Work unit = one (b, head) and TWO 128-row Q tiles (256 query rows) that
+// share every K/V tile loaded into shared memory.  The grid is persistent
+// (one CTA per SM); CTA c takes units c, c + G, c + 2G, ... so the CTAs
+// resident at any time work on neighbouring units of the same heads and K/V
+// is served from L2.
 //
 //   warps 0-3  softmax WG 0: thread t owns row t of Q tile 0 (TMEM lane t)
 //   warps 4-7  softmax WG 1: same for Q tile 1
-//   warp 8     TMA producer (one elected lane): Q0, Q1, then K0 V0 K1 V1 ...
-//   warp 9     MMA issuer (one lane) + TMEM allocator
+//   warp 8     TMA producer (one lane): Q0 Q1 | K0 V0 K1 V1 ... per unit
+//   warp 9     MMA issuer (whole warp, elect.sync issues) + TMEM allocator
+//   warp 10    O store warp: TMA-stores each staged O tile, frees the stage
+//   warp 11    idle (register donor)
 //
 // Tensor Memory (512 columns x 128 lanes x 32 bit):
 //   S0 [0,128)  S1 [128,256)  O0 [256,256+D)  O1 [256+D,256+2D)
@@ -28,6 +33,15 @@
 // in issue order, so when softmax WG q observes "S_q(j) complete" the
 // preceding PV_q(j-1) has completed too: the WG may rescale O_q in TMEM
 // without any further barrier, and P_q(j) may overwrite S_q(j)'s columns.
+// P is published in two halves (kv rows 0-63 / 64-127) so GEMM-II on the
+// first half overlaps the exponentials of the second.
+//
+// Across units: the producer loads the next unit's Q as soon as the last
+// S GEMMs of the current unit have completed (`q_empty`), the MMA warp
+// starts the next unit's S(0) while the softmax WGs run their epilogue, and
+// only the first PV of a unit waits for the epilogue to have drained O_q
+// from TMEM (`o_empty`).  The epilogue stages O in shared memory (the
+// swizzled TMA layout) and writes it with one TMA store per 64 columns.
 //
 // Rescaling is conditional (FlashAttention-4 style): a warp keeps its stale
 // row max unless some row's max grew by more than 2^8 in the exp2 domain.
@@ -44,22 +58,29 @@
 namespace fmha_b200 {
 
 struct FwdArgs {
-  void* o;                   // BSHD output, 16-bit
-  float* lse;                // [L][h][N] fp32 or nullptr
+  void* o;                   // BSHD output (direct-store epilogue of the d=256 kernel)
   int64_t o_sb, o_sn, o_sh;  // output strides (elements)
-  int N, H;
-  int n_kv_tiles;    // ceil(N / 128)
+  float* lse;        // [L][h][N] fp32 or nullptr
+  int N, H, L;
+  int n_kv_tiles;    // ceil(N / kBN)
+  int n_qblocks;     // Q blocks per head (256 rows for d<=128, 128 for d=256)
+  int n_units;       // L * H * n_qblocks
   float scale_log2;  // softmax scale * log2(e)
   float scale;       // softmax scale (natural)
   unsigned long long* trace;  // debug timeline (FMHA_TRACE=1) or nullptr
 };
 
-// Debug timeline for CTA (0,0,0): clock64 stamps written by one thread per
-// role.  trace[(q * n_kv + j) * 8 + k]:
+// Debug timeline for the first unit of CTA 0: clock64 stamps written by one
+// thread per role.  trace[(q * n_kv + j) * 8 + k]:
 //   k=0 softmax woke (S ready)  1 S in registers  2 row max done
 //   3 P stored + arrived        4 MMA saw P ready  5 MMA issued PV+S
+//   [6]/[7] of entry 0: kernel start / setup done; of the last tile:
+//   O ready / epilogue done.
+// Compiled in only with -DFMHA_TRACE_BUILD (tools/trace_timeline.py builds it).
 __device__ __forceinline__ void trace_stamp(const FwdArgs& a, bool on, int q, int j, int k) {
+#ifdef FMHA_TRACE_BUILD
   if (on) a.trace[(q * a.n_kv_tiles + j) * 8 + k] = clock64();
+#endif
 }
 
 template <int D>
@@ -72,58 +93,83 @@ struct FwdCfg {
   static constexpr int kKVTileBytes = kBN * D * 2;
   static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
   static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
-  static constexpr int kNumBars = 1 + 2 * kStages + 6;
-  static constexpr int kSmemBytes = kSmemQ + kSmemRing + kNumBars * 8 + 16;
+  static constexpr int kNumBars = 2 + 2 * kStages + 12;
+  static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
   static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
   static constexpr int kLoadWarp = 8;
   static constexpr int kMmaWarp = 9;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
+  static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
+
+// unit -> (b, head, q-block)
+__device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int& head, int& qb) {
+  qb = u % n_qb;
+  const int t = u / n_qb;
+  head = t % H;
+  b = t / H;
+}
 
 // kEmuPer16: of every 16 score pairs, how many take the FMA-pipe exp2.
 template <int D, bool kBF16, int kEmuPer16 = 0>
 __global__ void __launch_bounds__(384, 1)
     fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
-                          const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+                          const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmO, const FwdArgs args) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for the 128-B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
-  uint8_t* sRing = smem + C::kSmemQ;
+  uint8_t* sO = smem + C::kSmemQ;
+  uint8_t* sRing = sO + C::kSmemO;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing);
-  uint64_t* bar_q = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_full = p_full + 2;             // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* p_full = s_full + 2;             // [2][2]: (tile q, kv half)
+  uint64_t* o_full = p_full + 4;             // [2]
+  uint64_t* o_empty = o_full + 2;            // [2]
+  uint64_t* stage_free = o_empty + 2;        // O staging tile read by its TMA store
+  uint64_t* stage_ready = stage_free + 1;    // O staging tile written by a softmax WG
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int head = blockIdx.y;
-  const int b = blockIdx.z;
-  const int qrow0 = blockIdx.x * 2 * C::kBM;
   const int n_kv = args.n_kv_tiles;
-  const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#ifdef FMHA_TRACE_BUILD
+  const bool tr = args.trace != nullptr && blockIdx.x == 0;
+#else
+  constexpr bool tr = false;
+#endif
 
+#ifdef FMHA_TRACE_BUILD
+  const unsigned long long t_start = clock64();
+#endif
   if (threadIdx.x == 0) {
-    mbar_init(bar_q, 1);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&s_full[q], 1);
-      mbar_init(&p_full[q], 128);
+      mbar_init(&p_full[2 * q], 4);  // one arrival per softmax warp
+      mbar_init(&p_full[2 * q + 1], 4);
       mbar_init(&o_full[q], 1);
+      mbar_init(&o_empty[q], 4);
     }
+    mbar_init(stage_free, 1);
+    mbar_init(stage_ready, 4);
     fence_mbar_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
@@ -131,49 +177,64 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+#ifdef FMHA_TRACE_BUILD
+  if (threadIdx.x == 0 && tr) {
+    args.trace[6] = t_start;
+    args.trace[7] = clock64();
+  }
+#endif
 
   // Register split (setmaxnreg inside each role's branch so ptxas sees one
   // limit per region): the load/MMA warpgroup needs few registers, the
   // softmax warpgroups hold a 128-column S row plus packed P per thread.
   if (warp >= 8) {
     reg_dealloc<112>();
-  if (warp == C::kLoadWarp) {
-    // ---------------------------------------------------- TMA producer --
-    if (lane == 0) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      const uint64_t keep = l2_policy_evict_last();   // K/V re-read by sibling CTAs
-      const uint64_t once = l2_policy_evict_first();  // Q read once
-      mbar_arrive_expect_tx(bar_q, 2 * C::kQTileBytes);
+    if (warp == C::kLoadWarp) {
+      // -------------------------------------------------- TMA producer --
+      if (lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmO);
+        const uint64_t keep = l2_policy_evict_last();   // K/V re-read by sibling CTAs
+        const uint64_t once = l2_policy_evict_first();  // Q read once
+        int slot = 0;
+        uint32_t phase = 0;
+        int i = 0;
+        for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
+          int b, head, qb;
+          decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+          const int qrow0 = qb * 2 * C::kBM;
+          // Q smem is free once the previous unit's last S GEMMs completed
+          mbar_wait(q_empty, (i & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, 2 * C::kQTileBytes);
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
+          for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_4d_hint(&tmQ, bar_q, sQ + q * C::kQTileBytes + c * C::kBM * 128, c * 64, head,
-                           qrow0 + q * C::kBM, b, once);
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < n_kv; ++j) {
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_4d_hint(&tmQ, q_full, sQ + q * C::kQTileBytes + c * C::kBM * 128, c * 64,
+                               head, qrow0 + q * C::kBM, b, once);
+          for (int j = 0; j < n_kv; ++j) {
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&kv_empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
-          uint8_t* dst = sRing + slot * C::kKVTileBytes;
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait(&kv_empty[slot], phase ^ 1);
+              mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
+              uint8_t* dst = sRing + slot * C::kKVTileBytes;
 #pragma unroll
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_4d_hint(t == 0 ? &tmK : &tmV, &kv_full[slot], dst + c * C::kBN * 128, c * 64,
-                             head, j * C::kBN, b, keep);
-          if (++slot == C::kStages) {
-            slot = 0;
-            phase ^= 1;
+              for (int c = 0; c < C::kChunks; ++c)
+                tma_load_4d_hint(t == 0 ? &tmK : &tmV, &kv_full[slot], dst + c * C::kBN * 128,
+                                 c * 64, head, j * C::kBN, b, keep);
+              if (++slot == C::kStages) {
+                slot = 0;
+                phase ^= 1;
+              }
+            }
           }
         }
       }
-    }
-  } else if (warp == C::kMmaWarp) {
-    // ------------------------------------------------------ MMA issuer --
-    {  // whole warp: uniform control flow, one elected lane issues
+    } else if (warp == C::kMmaWarp) {
+      // ---------------------------------------------------- MMA issuer --
+      // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t kIdescQK = idesc_f16(kBF16, C::kBM, C::kBN, false, false);
       constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
       const uint32_t sQ_addr = smem_u32(sQ);
@@ -200,65 +261,98 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
           const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
           mma_ss_elect(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0 + off_a, 16, 1024),
-                 sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+                       sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
       // O_q (+)= P_q V : M=128, N=D, K=128 kv rows in 8 steps of 16 rows.
       // A = P from TMEM (8 columns per step); B = V, MN-major (d contiguous):
-      // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.
-      auto mma_pv = [&](int q, int vslot, bool accumulate) {
+      // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.  P arrives
+      // in two halves; each half's four MMAs start as soon as it is stored.
+      auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par) {
         const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
         const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
 #pragma unroll
-        for (int kk = 0; kk < C::kBN / 16; ++kk) {
-          mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
-                 sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
-                 (accumulate || kk > 0) ? 1u : 0u);
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(&p_full[2 * q + half], par);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = half * 4; kk < half * 4 + 4; ++kk) {
+            mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
+                         sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
+                         (accumulate || kk > 0) ? 1u : 0u);
+          }
         }
       };
 
-      mbar_wait(bar_q, 0);
-      int ks = next_slot();
-      tc_fence_after();
-      mma_qk(0, ks);
-      mma_commit_elect(&s_full[0]);
-      mma_qk(1, ks);
-      mma_commit_elect(&s_full[1]);
-      mma_commit_elect(&kv_empty[ks]);
-      for (int j = 1; j < n_kv; ++j) {
-        const int vs = next_slot();
-        ks = next_slot();
-        const uint32_t par = (j - 1) & 1;
-        mbar_wait(&p_full[0], par);
-        trace_stamp(args, tr, 0, j - 1, 4);
+      uint32_t it = 0;  // global K/V-tile counter (s_full / p_full parity)
+      int i = 0;
+      for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
+        const bool trm = tr && i == 0;
+        const uint32_t ue = (static_cast<uint32_t>(i) & 1) ^ 1;  // o_empty parity
+        mbar_wait(q_full, i & 1);
+        int ks = next_slot();
         tc_fence_after();
-        mma_pv(0, vs, j > 1);
         mma_qk(0, ks);
         mma_commit_elect(&s_full[0]);
-        trace_stamp(args, tr, 0, j - 1, 5);
-        mbar_wait(&p_full[1], par);
-        trace_stamp(args, tr, 1, j - 1, 4);
-        tc_fence_after();
-        mma_pv(1, vs, j > 1);
         mma_qk(1, ks);
         mma_commit_elect(&s_full[1]);
-        trace_stamp(args, tr, 1, j - 1, 5);
-        mma_commit_elect(&kv_empty[vs]);
+        if (n_kv == 1) mma_commit_elect(q_empty);
         mma_commit_elect(&kv_empty[ks]);
+        for (int j = 1; j < n_kv; ++j) {
+          const int vs = next_slot();
+          ks = next_slot();
+          const uint32_t par = it & 1;
+          mbar_wait(&p_full[0], par);
+          trace_stamp(args, trm, 0, j - 1, 4);
+          if (j == 1) mbar_wait(&o_empty[0], ue);  // previous unit's epilogue drained O0
+          mma_pv(0, vs, j > 1, par);
+          mma_qk(0, ks);
+          mma_commit_elect(&s_full[0]);
+          trace_stamp(args, trm, 0, j - 1, 5);
+          mbar_wait(&p_full[2], par);
+          trace_stamp(args, trm, 1, j - 1, 4);
+          if (j == 1) mbar_wait(&o_empty[1], ue);
+          mma_pv(1, vs, j > 1, par);
+          mma_qk(1, ks);
+          mma_commit_elect(&s_full[1]);
+          trace_stamp(args, trm, 1, j - 1, 5);
+          if (j == n_kv - 1) mma_commit_elect(q_empty);  // last reads of Q issued
+          mma_commit_elect(&kv_empty[vs]);
+          mma_commit_elect(&kv_empty[ks]);
+          ++it;
+        }
+        const int vs = next_slot();
+        const uint32_t par = it & 1;
+        if (n_kv == 1) mbar_wait(&o_empty[0], ue);
+        mma_pv(0, vs, n_kv > 1, par);
+        mma_commit_elect(&o_full[0]);
+        if (n_kv == 1) mbar_wait(&o_empty[1], ue);
+        mma_pv(1, vs, n_kv > 1, par);
+        mma_commit_elect(&o_full[1]);
+        mma_commit_elect(&kv_empty[vs]);
+        ++it;
       }
-      const int vs = next_slot();
-      const uint32_t par = (n_kv - 1) & 1;
-      mbar_wait(&p_full[0], par);
-      tc_fence_after();
-      mma_pv(0, vs, n_kv > 1);
-      mma_commit_elect(&o_full[0]);
-      mbar_wait(&p_full[1], par);
-      tc_fence_after();
-      mma_pv(1, vs, n_kv > 1);
-      mma_commit_elect(&o_full[1]);
-      mma_commit_elect(&kv_empty[vs]);
+    } else if (warp == 10) {
+      // ------------------------------------------------- O store warp --
+      // Uses of the staging tile alternate WG0, WG1 per unit: use k = 2i+q.
+      if (lane == 0) {
+        uint32_t k = 0;
+        for (int u = blockIdx.x; u < args.n_units; u += gridDim.x) {
+          int b, head, qb;
+          decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+          for (int q = 0; q < 2; ++q, ++k) {
+            mbar_wait(stage_ready, k & 1);
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_store_4d(&tmO, sO + c * C::kBM * 128, c * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
+            tma_store_commit();
+            tma_store_wait_read();
+            mbar_arrive(stage_free);
+          }
+        }
+        tma_store_wait_all();
+      }
     }
-  }
   } else {
     reg_alloc<192>();
     // ------------------------------------------------- softmax WG 0 / 1 --
@@ -269,102 +363,123 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tO = tmem + lane_off + (q ? C::kColO1 : C::kColO0);
     const float sl2 = args.scale_log2;
     const int N = args.N;
-    float m = -INFINITY;  // running max in raw score units
-    float l = 0.0f;       // running sum of exp2((s - m) * sl2)
+    uint32_t it = 0;
+    int i = 0;
+    for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
+      int b, head, qb;
+      decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+      const bool trq = tr && i == 0 && r == 0;
+      float m = -INFINITY;  // running max in raw score units
+      float l = 0.0f;       // running sum of exp2((s - m) * sl2)
 
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[q], j & 1);
-      const bool trr = tr && r == 0;
-      trace_stamp(args, trr, q, j, 0);
-      tc_fence_after();
-      uint32_t sr[128];
-      tmem_ld32x32b_x128(tS, sr);
-      trace_stamp(args, trr, q, j, 1);
-      float s[128];
+      for (int j = 0; j < n_kv; ++j, ++it) {
+        mbar_wait(&s_full[q], it & 1);
+        trace_stamp(args, trq, q, j, 0);
+        tc_fence_after();
+        uint32_t sr[128];
+        tmem_ld32x32b_x128(tS, sr);
+        trace_stamp(args, trq, q, j, 1);
+        float s[128];
 #pragma unroll
-      for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
-      const int valid = N - j * C::kBN;  // columns >= valid are padding
-      if (valid < C::kBN) {
+        for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
+        const int valid = N - j * C::kBN;  // columns >= valid are padding
+        if (valid < C::kBN) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c >= valid) s[c] = -INFINITY;
-      }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-      for (int c = 4; c < 128; c += 4) {
-        mx0 = fmaxf(mx0, s[c]);
-        mx1 = fmaxf(mx1, s[c + 1]);
-        mx2 = fmaxf(mx2, s[c + 2]);
-        mx3 = fmaxf(mx3, s[c + 3]);
-      }
-      const float m_new = fmaxf(m, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
-      trace_stamp(args, trr, q, j, 2);
-      const bool need = (m_new - m) * sl2 > 8.0f;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = ex2_approx((m - m_new) * sl2);
-        l *= alpha;
-        if (j > 0) {
-          // O_q(j-1) is complete (see header); rescale this lane's row
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32x32b_x32(tO + c * 32, o);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32x32b_x32(tO + c * 32, o);
-          }
+          for (int c = 0; c < 128; ++c)
+            if (c >= valid) s[c] = -INFINITY;
         }
-        m = m_new;
-      }
-      const float neg = -m * sl2;
-      // exponentiate and store P in two 64-column halves (32 packed columns
-      // each) so only half of P is live in registers at a time
-      float rowsum;
-      {
+        // row max with 8 independent chains (short dependency depth)
+        float mx[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
+#pragma unroll
+        for (int c = 16; c < 128; c += 16)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
+        const float m_new = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                  fmaxf(fmaxf(mx[4], mx[5]), fmaxf(fmaxf(mx[6], mx[7]), m)));
+        // Conditional rescale: keep the stale max unless some row of this
+        // warp grew by more than 8 (log2 units).  S_q(j) observed =>
+        // PV_q(j-1) done, so O_q may be rescaled in TMEM here.
+        if (__any_sync(0xffffffffu, (m_new - m) * sl2 > 8.0f)) {
+          const float alpha = ex2_approx((m - m_new) * sl2);
+          l *= alpha;
+          if (j > 0) {
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              tmem_ld32x32b_x32(tO + c * 32, o);
+#pragma unroll
+              for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+              tmem_st32x32b_x32(tO + c * 32, o);
+            }
+          }
+          m = m_new;
+        }
+        trace_stamp(args, trq, q, j, 2);
+        const float neg = -m * sl2;
+        // exponentiate and store P in two 64-column halves (32 packed
+        // columns each), each published to the MMA warp as soon as it is in
+        // TMEM (one arrival per warp)
+        auto publish = [&](const uint32_t(&p)[32], int half) {
+          tmem_st32x32b_x32(tS + half * 32, p);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[2 * q + half]);
+        };
         uint32_t p[32];
-        rowsum = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
-                                : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
-        tmem_st32x32b_x32(tS, p);
-      }
-      {
-        uint32_t p[32];
+        float rowsum = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
+                                      : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
+        publish(p, 0);
         rowsum += valid < C::kBN ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p)
                                  : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p);
-        tmem_st32x32b_x32(tS + 32, p);
+        publish(p, 1);
+        l += rowsum;
+        trace_stamp(args, trq, q, j, 3);
       }
-      l += rowsum;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[q]);
-      trace_stamp(args, trr, q, j, 3);
-    }
 
-    // ------------------------------------------------------- epilogue --
-    mbar_wait(&o_full[q], 0);
-    tc_fence_after();
-    const int row = qrow0 + q * C::kBM + r;
-    const bool row_ok = row < N;
-    const float inv = 1.0f / l;
-    uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
-                     static_cast<int64_t>(row_ok ? row : 0) * args.o_sn +
-                     static_cast<int64_t>(head) * args.o_sh;
+      // ----------------------------------------------------- epilogue --
+      // O_q -> registers -> x(1/Sigma) (rowwise_finalize) -> 16-bit -> the
+      // swizzled staging tile -> TMA store; TMEM is released as soon as it
+      // has been read so the next unit's first PV can start.
+      mbar_wait(&o_full[q], i & 1);
+      tc_fence_after();
+      trace_stamp(args, trq, q, n_kv - 1, 6);
+      // The two WGs take the staging tile in turn (WG0 unit i, WG1 unit i,
+      // WG0 unit i+1, ...): wait until the previous user's TMA store has
+      // read it.  Completion #k of stage_free is the k-th use, so WG0 waits
+      // for odd completions and WG1 for even ones.
+      mbar_wait(stage_free, q ? 0u : 1u);
+      const float inv = 1.0f / l;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32x32b_x32(tO + c * 32, o);  // warp-collective: every lane loads
-      uint32_t h2[16];
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32x32b_x32(tO + c * 32, o);
+        uint32_t h2[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        h2[i] = pack2<kBF16>(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-      if (row_ok) {
+        for (int t = 0; t < 16; ++t)
+          h2[t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+        // columns c*32 .. c*32+31 = four 16-B units of 64-column atom c/2
+        uint8_t* rowp = sO + (c >> 1) * (C::kBM * 128) + r * 128;
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          st_global_v4(orow + c * 32 + v * 8, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2],
-                       h2[4 * v + 3]);
+        for (int v = 0; v < 4; ++v) {
+          const int unit = ((c & 1) * 4 + v) ^ (r & 7);  // 128-B swizzle
+          st_shared_v4(rowp + unit * 16, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2], h2[4 * v + 3]);
+        }
       }
+      tc_fence_before();
+      fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&o_empty[q]);   // O_q drained from TMEM
+        mbar_arrive(stage_ready);   // this warp's 32 rows staged
+      }
+      const int row = qb * 2 * C::kBM + q * C::kBM + r;
+      if (row < N && args.lse != nullptr)
+        args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
+      trace_stamp(args, trq, q, n_kv - 1, 7);
     }
-    if (row_ok && args.lse != nullptr)
-      args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
   }
 
   tc_fence_before();
