@@ -104,11 +104,11 @@ int num_sms() {
   return n;
 }
 
-template <int D, bool BF16, int EMU = 0>
+template <int D, bool BF16, int EMU = 0, bool ORDER = false>
 fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st) {
   using Cfg = fmha_b200::FwdCfg<D>;
-  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
+  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU, ORDER>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -253,29 +253,49 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool bf = p->dtype == FMHA_BF16;
   switch (p->d) {
-    case 64:
-      return bf ? launch_d128<64, true>(p, mq, mk, mv, mo, lse, st)
-                : launch_d128<64, false>(p, mq, mk, mv, mo, lse, st);
+    case 64: {
+      static const int emu64 = [] {
+        const char* e = std::getenv("FMHA_TUNE_EMU64");
+        return e ? std::atoi(e) : 4;
+      }();
+      if (emu64 == 0)
+        return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st);
+      if (emu64 == 10)  // tuning: softmax WGs take turns on MUFU, all-MUFU exp
+        return bf ? launch_d128<64, true, 0, true>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 0, true>(p, mq, mk, mv, mo, lse, st);
+      if (emu64 == 14)  // tuning: turns + 4/16 polynomial exp
+        return bf ? launch_d128<64, true, 4, true>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 4, true>(p, mq, mk, mv, mo, lse, st);
+      if (emu64 == 6)
+        return bf ? launch_d128<64, true, 6>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 6>(p, mq, mk, mv, mo, lse, st);
+      if (emu64 == 8)
+        return bf ? launch_d128<64, true, 8>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 8>(p, mq, mk, mv, mo, lse, st);
+      return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st)
+                : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st);
+    }
     case 128: {
-      // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default: all MUFU)
+      // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default 4 of 16 pairs)
       static const int emu = [] {
         const char* e = std::getenv("FMHA_TUNE_EMU");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 4;
       }();
       if (emu == 0)
         return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
-      if (emu == 4)
-        return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
-      if (emu == 8)
-        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st);
+      if (emu == 12)  // tuning: emu 4 with the softmax WGs taking turns on MUFU
+        return bf ? launch_d128<128, true, 4, true>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 4, true>(p, mq, mk, mv, mo, lse, st);
+      if (emu == 8)  // tuning: emu 0 with the softmax WGs taking turns on MUFU
+        return bf ? launch_d128<128, true, 0, true>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 0, true>(p, mq, mk, mv, mo, lse, st);
       if (emu == 6)
         return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st);
-      return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
-                : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
+      return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
+                : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
     default:
       return bf ? launch_d256<true>(p, mq, mk, mv, o, lse, st)

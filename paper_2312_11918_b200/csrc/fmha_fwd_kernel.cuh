@@ -92,10 +92,11 @@ struct FwdCfg {
   static constexpr int kQTileBytes = kBM * D * 2;
   static constexpr int kKVTileBytes = kBN * D * 2;
   static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
-  static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kQStages = D == 64 ? 2 : 1;  // Q double-buffered when it fits
+  static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
   static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
-  static constexpr int kNumBars = 2 + 2 * kStages + 12;
+  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 14;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
   static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
@@ -115,7 +116,7 @@ __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int&
 }
 
 // kEmuPer16: of every 16 score pairs, how many take the FMA-pipe exp2.
-template <int D, bool kBF16, int kEmuPer16 = 0>
+template <int D, bool kBF16, int kEmuPer16 = 0, bool kOrderExp = false>
 __global__ void __launch_bounds__(384, 1)
     fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -130,9 +131,9 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sO = smem + C::kSmemQ;
   uint8_t* sRing = sO + C::kSmemO;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
+  uint64_t* q_full = bars;               // [kQStages]
+  uint64_t* q_empty = bars + C::kQStages;  // [kQStages]
+  uint64_t* kv_full = bars + 2 * C::kQStages;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
   uint64_t* p_full = s_full + 2;             // [2][2]: (tile q, kv half)
@@ -140,7 +141,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* o_empty = o_full + 2;            // [2]
   uint64_t* stage_free = o_empty + 2;        // O staging tile read by its TMA store
   uint64_t* stage_ready = stage_free + 1;    // O staging tile written by a softmax WG
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 1);
+  uint64_t* exp_turn = stage_ready + 1;      // [2]: softmax WGs take turns on MUFU
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(exp_turn + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -155,8 +157,10 @@ __global__ void __launch_bounds__(384, 1)
   const unsigned long long t_start = clock64();
 #endif
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int s = 0; s < C::kQStages; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -170,6 +174,8 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_init(stage_free, 1);
     mbar_init(stage_ready, 4);
+    mbar_init(&exp_turn[0], 4);
+    mbar_init(&exp_turn[1], 4);
     fence_mbar_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
@@ -205,15 +211,19 @@ __global__ void __launch_bounds__(384, 1)
           int b, head, qb;
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
           const int qrow0 = qb * 2 * C::kBM;
-          // Q smem is free once the previous unit's last S GEMMs completed
-          mbar_wait(q_empty, (i & 1) ^ 1);
-          mbar_arrive_expect_tx(q_full, 2 * C::kQTileBytes);
+          // Q stage is free once the last S GEMMs of the unit that used it
+          // before have completed
+          const int qs = i % C::kQStages;
+          const uint32_t qph = static_cast<uint32_t>(i / C::kQStages) & 1;
+          mbar_wait(&q_empty[qs], qph ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], 2 * C::kQTileBytes);
+          uint8_t* sQs = sQ + qs * 2 * C::kQTileBytes;
 #pragma unroll
           for (int q = 0; q < 2; ++q)
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
-              tma_load_4d_hint(&tmQ, q_full, sQ + q * C::kQTileBytes + c * C::kBM * 128, c * 64,
-                               head, qrow0 + q * C::kBM, b, once);
+              tma_load_4d_hint(&tmQ, &q_full[qs], sQs + q * C::kQTileBytes + c * C::kBM * 128,
+                               c * 64, head, qrow0 + q * C::kBM, b, once);
           for (int j = 0; j < n_kv; ++j) {
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(384, 1)
       // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t kIdescQK = idesc_f16(kBF16, C::kBM, C::kBN, false, false);
       constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
-      const uint32_t sQ_addr = smem_u32(sQ);
+      uint32_t sQ_addr = smem_u32(sQ);
       const uint32_t ring_addr = smem_u32(sRing);
       int slot = 0;
       uint32_t phase = 0;
@@ -289,14 +299,16 @@ __global__ void __launch_bounds__(384, 1)
       for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
         const bool trm = tr && i == 0;
         const uint32_t ue = (static_cast<uint32_t>(i) & 1) ^ 1;  // o_empty parity
-        mbar_wait(q_full, i & 1);
+        const int qs = i % C::kQStages;
+        mbar_wait(&q_full[qs], static_cast<uint32_t>(i / C::kQStages) & 1);
+        sQ_addr = smem_u32(sQ) + qs * 2 * C::kQTileBytes;
         int ks = next_slot();
         tc_fence_after();
         mma_qk(0, ks);
         mma_commit_elect(&s_full[0]);
         mma_qk(1, ks);
         mma_commit_elect(&s_full[1]);
-        if (n_kv == 1) mma_commit_elect(q_empty);
+        if (n_kv == 1) mma_commit_elect(&q_empty[qs]);
         mma_commit_elect(&kv_empty[ks]);
         for (int j = 1; j < n_kv; ++j) {
           const int vs = next_slot();
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(384, 1)
           mma_qk(1, ks);
           mma_commit_elect(&s_full[1]);
           trace_stamp(args, trm, 1, j - 1, 5);
-          if (j == n_kv - 1) mma_commit_elect(q_empty);  // last reads of Q issued
+          if (j == n_kv - 1) mma_commit_elect(&q_empty[qs]);  // last reads of Q issued
           mma_commit_elect(&kv_empty[vs]);
           mma_commit_elect(&kv_empty[ks]);
           ++it;
@@ -388,39 +400,34 @@ __global__ void __launch_bounds__(384, 1)
           for (int c = 0; c < 128; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        // row max with 8 independent chains (short dependency depth)
-        float mx[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
-#pragma unroll
-        for (int c = 16; c < 128; c += 16)
-#pragma unroll
-          for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
-        const float m_new = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                  fmaxf(fmaxf(mx[4], mx[5]), fmaxf(fmaxf(mx[6], mx[7]), m)));
-        // Conditional rescale: keep the stale max unless some row of this
-        // warp grew by more than 8 (log2 units).  S_q(j) observed =>
-        // PV_q(j-1) done, so O_q may be rescaled in TMEM here.
-        if (__any_sync(0xffffffffu, (m_new - m) * sl2 > 8.0f)) {
+        // Rescale O_q (TMEM) and the running sum by 2^((m - m_new) c); only
+        // called while O_q is quiescent (see the call sites).
+        auto rescale = [&](float m_new) {
           const float alpha = ex2_approx((m - m_new) * sl2);
           l *= alpha;
-          if (j > 0) {
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-              uint32_t o[32];
-              tmem_ld32x32b_x32(tO + c * 32, o);
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32x32b_x32(tO + c * 32, o);
 #pragma unroll
-              for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-              tmem_st32x32b_x32(tO + c * 32, o);
-            }
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32x32b_x32(tO + c * 32, o);
           }
           m = m_new;
-        }
-        trace_stamp(args, trq, q, j, 2);
-        const float neg = -m * sl2;
-        // exponentiate and store P in two 64-column halves (32 packed
-        // columns each), each published to the MMA warp as soon as it is in
-        // TMEM (one arrival per warp)
+        };
+        // full row max, 8 independent chains (short dependency depth)
+        auto row_max = [&]() {
+          float mx[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
+#pragma unroll
+          for (int c = 16; c < 128; c += 16)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
+          return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        };
+        // publish half h of P (32 packed columns) to the MMA warp
         auto publish = [&](const uint32_t(&p)[32], int half) {
           tmem_st32x32b_x32(tS + half * 32, p);
           tmem_wait_st();
@@ -428,14 +435,38 @@ __global__ void __launch_bounds__(384, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[2 * q + half]);
         };
+        // The two WGs take turns on the exponential unit (WG0 tile t, WG1
+        // tile t, WG0 tile t+1, ...): the WG on the critical path never
+        // shares MUFU throughput, and each WG's non-exp work (TMEM load,
+        // publishing, waiting for the next S) hides under the other's turn.
+        if (kOrderExp) mbar_wait(&exp_turn[q], q ? (it & 1) : ((it & 1) ^ 1));
+        // Row max first (8 chains), then exponentiate against the running
+        // max.  Conditional rescale: keep the stale max unless some row of
+        // this warp grew by more than 8 (log2 units), i.e. P stays <= 256.
+        // S_q(j) observed => PV_q(j-1) complete, so O_q may be rescaled here.
+        {
+          const float m_new = fmaxf(row_max(), m);
+          if (__any_sync(0xffffffffu, (m_new - m) * sl2 > 8.0f)) {
+            if (j == 0)
+              m = m_new;  // l = 0 and the first PV overwrites O
+            else
+              rescale(m_new);
+          }
+        }
+        const float neg = -m * sl2;
         uint32_t p[32];
-        float rowsum = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
-                                      : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
+        const float rs_a = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
+                                          : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
         publish(p, 0);
-        rowsum += valid < C::kBN ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p)
-                                 : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p);
+        trace_stamp(args, trq, q, j, 2);
+        const float rs_b = valid < C::kBN ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p)
+                                          : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p);
+        if (kOrderExp) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&exp_turn[q ^ 1]);
+        }
         publish(p, 1);
-        l += rowsum;
+        l += rs_a + rs_b;
         trace_stamp(args, trq, q, j, 3);
       }
 

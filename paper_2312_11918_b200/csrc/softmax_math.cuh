@@ -108,42 +108,6 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
   return (a0 + b0) + (a1 + b1);
 }
 
-// Same as exp_rowsum_pack, and also returns the max of the raw scores
-// s[kOff .. kOff+kCols) (FMNMX3 on the ALU pipe, interleaved with the
-// exponentials so it costs no extra latency).
-template <bool kBF16, int kOff, int kCols, int kEmuPer16, int kTotal>
-__device__ __forceinline__ float exp_rowsum_pack_max(const float (&s)[kTotal], float c, float neg_mc,
-                                                     uint32_t (&p)[kCols / 2], float& mx_out) {
-  const uint64_t c2 = f2_pack(c, c);
-  const uint64_t nm2 = f2_pack(neg_mc, neg_mc);
-  uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = f2_pack(0.f, 0.f);
-  float mx0 = s[kOff], mx1 = s[kOff + 1], mx2 = s[kOff + 2], mx3 = s[kOff + 3];
-#pragma unroll
-  for (int i = 0; i < kCols / 2; ++i) {
-    const float a = s[kOff + 2 * i], b = s[kOff + 2 * i + 1];
-    if ((i & 1) == 0)
-      mx0 = fmaxf(mx0, fmaxf(a, b));
-    else if ((i & 3) == 1)
-      mx1 = fmaxf(mx1, fmaxf(a, b));
-    else if ((i & 7) == 3)
-      mx2 = fmaxf(mx2, fmaxf(a, b));
-    else
-      mx3 = fmaxf(mx3, fmaxf(a, b));
-    const uint64_t x = ffma2(f2_pack(a, b), c2, nm2);
-    const uint64_t e = ((i & 15) < kEmuPer16) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
-    if (i & 1)
-      acc1 = fadd2(acc1, e);
-    else
-      acc0 = fadd2(acc0, e);
-    p[i] = pack2_x2<kBF16>(e);
-  }
-  mx_out = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-  float a0, a1, b0, b1;
-  f2_unpack(acc0, a0, a1);
-  f2_unpack(acc1, b0, b1);
-  return (a0 + b0) + (a1 + b1);
-}
-
 template <uint32_t kRegs>
 __device__ __forceinline__ void reg_alloc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegs));

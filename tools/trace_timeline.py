@@ -33,8 +33,11 @@ for j in range(min(n_kv, 12)):
         r = t[qq, j]
         print(f"{qq} {j:2d} | " + " ".join(f"{x:10d}" for x in r[:6]) +
               f" | {r[1]-r[0]:4d} {r[2]-r[1]:4d} {r[3]-r[2]:5d} {r[4]-r[3]:6d} {r[5]-r[4]:5d}")
-per = np.diff(t[0, 2:n_kv - 1, 0])
-print("steady-state period per K/V tile (clk): median", int(np.median(per)), "min", int(per.min()))
+if n_kv > 3:
+    per = np.diff(t[0, 2:n_kv - 1, 0])
+    print("steady-state period per K/V tile (clk): median", int(np.median(per)), "min", int(per.min()))
+if n_kv <= 3:
+    sys.exit(0)
 d_ld = np.median(t[:, 2:-1, 1] - t[:, 2:-1, 0]); d_max = np.median(t[:, 2:-1, 2] - t[:, 2:-1, 1])
 d_exp = np.median(t[:, 2:-1, 3] - t[:, 2:-1, 2]); d_p2m = np.median(t[:, 2:-2, 4] - t[:, 2:-2, 3])
 d_iss = np.median(t[:, 2:-2, 5] - t[:, 2:-2, 4])
