@@ -6,10 +6,17 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2312_11918_b200
 LIB := $(PKG)/libfmha_b200.so
-SRCS := $(PKG)/csrc/fmha_api.cu $(PKG)/csrc/fmha_host.cpp
+SRCS := $(PKG)/csrc/fmha_api.cu $(PKG)/csrc/fmha_reference.cu $(PKG)/csrc/fmha_host.cpp $(PKG)/csrc/fmha_io.cpp
 HDRS := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp include/fmha/*.h include/fmha/*.hpp)
 
-all: $(LIB) oracle
+CLI := $(PKG)/fmha-b200
+
+all: $(LIB) $(CLI) oracle
+
+# the C++ CLI (reference fmha-sim counterpart), linked against the library
+$(CLI): $(PKG)/csrc/fmha_cli.cpp $(LIB) include/fmha/fmha.h include/fmha/fmha.hpp
+	$(NVCC) -std=c++20 -O2 -o $@ $(PKG)/csrc/fmha_cli.cpp -L$(PKG) -lfmha_b200 -Xlinker -rpath -Xlinker '$$ORIGIN'
+
 
 $(PKG)/csrc/tmem_ops.cuh: tools/gen_tmem_ops.py
 	python tools/gen_tmem_ops.py
@@ -33,7 +40,7 @@ build:
 $(LIB): | build
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean trace

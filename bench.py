@@ -193,8 +193,8 @@ def run_reference(args):
         orc.build()
     cfg, local, scaling, global_L = workload(args.config, 1, 0)
     threads = orc.default_threads()
-    # per-step sample sized so W + K steps stay within ~3 minutes
-    per_step_budget = 180.0 / max(1, args.steps + args.warmup)
+    # per-step sample sized so W + K steps stay within ~2 minutes
+    per_step_budget = 120.0 / max(1, args.steps + args.warmup)
     probe = cpu_baseline(cfg, threads, mode="1")
     tiles_per_thread = max(1, int(per_step_budget / max(probe["seconds"], 1e-3)))
     for _ in range(args.warmup):

@@ -104,6 +104,26 @@ fmha_status fmha_forward_f32(const float* q, const float* k, const float* v, int
                              int64_t h, int64_t d, int64_t bM, int64_t bN, fmha_dtype dtype,
                              float scale, float* o, float* lse, int device);
 
+/*
+ * Verification path (NOT the hot path): an independent fp32 CUDA-core
+ * attention with the reference's standard_attention semantics
+ * (attention.cpp:137-151; exact expf, unrounded P).  q, k, v: 16-bit device
+ * tensors described by `p`; o: dense fp32 [L][N][h][d] device buffer; lse:
+ * [L][h][N] or NULL.  Used by the `fmha-b200 verify` CLI as its checker.
+ */
+fmha_status fmha_fwd_reference(const fmha_fwd_params* p, const void* q, const void* k,
+                               const void* v, float* o, float* lse, void* cuda_stream);
+
+/*
+ * FHMT fixture files -- the reference's save_tensor / load_tensor format
+ * (tensor.hpp:36-38, tensor.cpp:30-84): magic "FHMT", version 1, int64
+ * L, N, h, d, precision tag (0 f32, 1 f16), values in (b, n, head, k) order.
+ */
+fmha_status fmha_tensor_save(const char* path, const float* data, int64_t L, int64_t N, int64_t h,
+                             int64_t d, int f16);
+fmha_status fmha_tensor_load_header(const char* path, int64_t dims[4], int* f16);
+fmha_status fmha_tensor_load(const char* path, float* data, int64_t count);
+
 /* 4 * N^2 * d * h * L (attention_flops, attention.cpp:191-193). */
 int64_t fmha_attention_flops(int64_t L, int64_t N, int64_t h, int64_t d);
 

@@ -7,6 +7,7 @@
 //   Tensor4 fmha_forward(const AttentionProblem&, const TileConfig&,
 //                        Precision prec = Precision::ExactF32);        :58-59
 //   int64_t attention_flops(int64_t L, int64_t N, int64_t h, int64_t d); :78
+//   void save_tensor(...) / Tensor4 load_tensor(...)   (tensor.hpp:36-38)
 // and Tensor4 (include/fmhasim/tensor.hpp:12-32).
 //
 // A reference caller switches `fmhasim::` to `fmha_b200::` and the include
@@ -81,5 +82,10 @@ Tensor4 fmha_forward(const AttentionProblem& p, const TileConfig& t, Precision p
                      std::vector<float>* lse, int device = 0);
 
 int64_t attention_flops(int64_t L, int64_t N, int64_t h, int64_t d);
+
+// FHMT fixture I/O, same format and exceptions as the reference's
+// save_tensor / load_tensor (tensor.hpp:36-38): precision "f32" or "f16".
+void save_tensor(const Tensor4& t, const std::string& path, const std::string& precision = "f32");
+Tensor4 load_tensor(const std::string& path);
 
 }  // namespace fmha_b200

@@ -88,6 +88,8 @@ def ref():
         R.ref_fmha_forward_heads.argtypes = [_f32p, _f32p, _f32p] + [_i64] * 5 + [_f32p, C.c_int]
         R.ref_fmha_tiles.argtypes = [_f32p, _f32p, _f32p] + [_i64] * 6 + [
             C.c_int, _i64p, _i64, _f32p, _f32p, C.c_int]
+        R.ref_save_tensor.argtypes = [C.c_char_p, _f32p] + [_i64] * 4 + [C.c_int]
+        R.ref_load_tensor.argtypes = [C.c_char_p, _f32p, _i64, _i64p]
         _ref = R
     return _ref
 
@@ -224,3 +226,19 @@ def ref_fmha_forward_heads(qh, kh, vh, bM=128, bN=128, threads=None):
     out = np.empty_like(qh)
     ref().ref_fmha_forward_heads(qh, kh, vh, H, N, d, bM, bN, out, threads or default_threads())
     return out
+
+
+def ref_save_tensor(path, t, f16=False):
+    t = np.ascontiguousarray(t, np.float32)
+    L, N, h, d = t.shape
+    return ref().ref_save_tensor(path.encode(), t.reshape(-1), L, N, h, d, int(f16))
+
+
+def ref_load_tensor(path, capacity=1 << 24):
+    out = np.empty(capacity, np.float32)
+    dims = np.zeros(4, np.int64)
+    st = ref().ref_load_tensor(path.encode(), out, capacity, dims)
+    if st:
+        raise RuntimeError("reference load_tensor failed")
+    L, N, h, d = (int(x) for x in dims)
+    return out[: L * N * h * d].reshape(L, N, h, d).copy()

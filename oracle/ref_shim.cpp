@@ -147,4 +147,30 @@ int ref_fmha_tiles(const float* q, const float* k, const float* v, int64_t L, in
   }
 }
 
+// save_tensor / load_tensor (tensor.cpp:30-84) for the FHMT cross-compat test.
+int ref_save_tensor(const char* path, const float* data, int64_t L, int64_t N, int64_t h, int64_t d,
+                    int f16) {
+  try {
+    save_tensor(from_buf(data, L, N, h, d), path, f16 ? "f16" : "f32");
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+int ref_load_tensor(const char* path, float* out, int64_t capacity, int64_t* dims) {
+  try {
+    Tensor4 t = load_tensor(path);
+    dims[0] = t.L;
+    dims[1] = t.N;
+    dims[2] = t.h;
+    dims[3] = t.d;
+    if (t.elements() > capacity) return 3;
+    std::memcpy(out, t.data.data(), sizeof(float) * t.data.size());
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
 }  // extern "C"

@@ -24,8 +24,8 @@ import os
 
 import numpy as np
 
-__all__ = ["lib", "fmha_forward", "fmha_fwd", "fmha_fwd_host", "attention_flops", "FmhaError",
-           "LIB_PATH", "F16", "BF16"]
+__all__ = ["lib", "fmha_forward", "fmha_fwd", "fmha_fwd_host", "fmha_fwd_reference", "attention_flops",
+           "save_tensor", "load_tensor", "FmhaError", "LIB_PATH", "CLI_PATH", "F16", "BF16"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 # FMHA_B200_LIB selects an alternative build (e.g. build/libfmha_b200_trace.so)
@@ -79,6 +79,14 @@ def lib():
         L.fmha_host_f32_to_16.restype = C.c_uint16
         L.fmha_host_16_to_f32.argtypes = [C.c_uint16, C.c_int]
         L.fmha_host_16_to_f32.restype = C.c_float
+        L.fmha_tensor_save.argtypes = [C.c_char_p, vp] + [C.c_int64] * 4 + [C.c_int]
+        L.fmha_tensor_save.restype = C.c_int
+        L.fmha_tensor_load_header.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+        L.fmha_tensor_load_header.restype = C.c_int
+        L.fmha_tensor_load.argtypes = [C.c_char_p, vp, C.c_int64]
+        L.fmha_tensor_load.restype = C.c_int
+        L.fmha_fwd_reference.argtypes = [P, vp, vp, vp, vp, vp, vp]
+        L.fmha_fwd_reference.restype = C.c_int
         _lib = L
     return _lib
 
@@ -189,6 +197,55 @@ def fmha_fwd_host(q, k, v, o, lse=None, dtype=F16, scale=None, device=0):
     if st:
         _raise(st)
     return o, lse
+
+
+def save_tensor(t, path, precision="f32"):
+    """FHMT fixture file (the reference's save_tensor, tensor.cpp:30-60)."""
+    if precision not in ("f32", "f16"):
+        raise ValueError("save_tensor: unknown precision " + str(precision))
+    t = np.ascontiguousarray(t, np.float32)
+    if t.ndim != 4:
+        raise ValueError("expected a (L,N,h,d) array")
+    L, N, h, d = t.shape
+    st = lib().fmha_tensor_save(str(path).encode(), t.ctypes.data, L, N, h, d, int(precision == "f16"))
+    if st:
+        raise RuntimeError(lib().fmha_last_error().decode())
+
+
+def load_tensor(path):
+    """Read an FHMT fixture file (the reference's load_tensor, tensor.cpp:62-84)."""
+    dims = (C.c_int64 * 4)()
+    f16 = C.c_int(0)
+    if lib().fmha_tensor_load_header(str(path).encode(), dims, C.byref(f16)):
+        raise RuntimeError(lib().fmha_last_error().decode())
+    out = np.empty(tuple(int(x) for x in dims), np.float32)
+    if lib().fmha_tensor_load(str(path).encode(), out.ctypes.data, out.size):
+        raise RuntimeError(lib().fmha_last_error().decode())
+    return out
+
+
+def fmha_fwd_reference(q, k, v, scale=None):
+    """Verification path: the fp32 CUDA-core standard attention
+    (attention.cpp:137-151 semantics) on torch CUDA 16-bit tensors.
+    Returns fp32 (O (L, N, h, d), LSE (L, h, N))."""
+    import torch
+    L, N, h, d = q.shape
+    p = FwdParams()
+    p.L, p.N, p.h, p.d = L, N, h, d
+    p.q_stride, p.k_stride, p.v_stride, p.o_stride = (_strides(q, "q"), _strides(k, "k"),
+                                                      _strides(v, "v"), (C.c_int64 * 3)(N * h * d, h * d, d))
+    p.scale = float(scale or 0.0)
+    p.dtype = BF16 if q.dtype == torch.bfloat16 else F16
+    o = torch.empty((L, N, h, d), dtype=torch.float32, device=q.device)
+    lse = torch.empty((L, h, N), dtype=torch.float32, device=q.device)
+    st = lib().fmha_fwd_reference(C.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                  lse.data_ptr(), torch.cuda.current_stream(q.device).cuda_stream)
+    if st:
+        _raise(st)
+    return o, lse
+
+
+CLI_PATH = os.path.join(HERE, "fmha-b200")
 
 
 def launch_count() -> int:

@@ -173,7 +173,7 @@ struct Workspace {
   std::mutex mu;
   void* dev = nullptr;
   size_t bytes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t streams[2] = {nullptr, nullptr};
 };
 Workspace& workspace(int device) {
   static Workspace ws[64];
@@ -321,10 +321,9 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   std::lock_guard<std::mutex> lock(ws.mu);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  if (!ws.stream) {
-    e = cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-  }
+  for (auto& st : ws.streams)
+    if (!st && (e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
   if (ws.bytes < total) {
     if (ws.dev) cudaFree(ws.dev);
     ws.dev = nullptr;
@@ -339,17 +338,35 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   char* dv = dk + up(nk);
   char* dO = dv + up(nv);
   float* dl = lse ? reinterpret_cast<float*>(dO + up(no)) : nullptr;
-  if ((e = cudaMemcpyAsync(dq, q, nq, cudaMemcpyHostToDevice, ws.stream)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(dk, k, nk, cudaMemcpyHostToDevice, ws.stream)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(dv, v, nv, cudaMemcpyHostToDevice, ws.stream)) != cudaSuccess)
-    return cuda_fail(e, "cudaMemcpyAsync H2D");
-  s = fmha_fwd(p, dq, dk, dv, dO, dl, ws.stream);
-  if (s != FMHA_OK) return s;
-  if ((e = cudaMemcpyAsync(o, dO, no, cudaMemcpyDeviceToHost, ws.stream)) != cudaSuccess)
-    return cuda_fail(e, "cudaMemcpyAsync D2H");
-  if (lse && (e = cudaMemcpyAsync(lse, dl, nl, cudaMemcpyDeviceToHost, ws.stream)) != cudaSuccess)
-    return cuda_fail(e, "cudaMemcpyAsync D2H lse");
-  if ((e = cudaStreamSynchronize(ws.stream)) != cudaSuccess) return cuda_fail(e, "kernel execution");
+  // Batch chunks alternate between two streams so the H2D copy of chunk c+1
+  // overlaps the kernel and the D2H copy of chunk c (copy engines and SMs
+  // work concurrently); each chunk is an independent sub-problem.
+  const int64_t n_chunks = std::min<int64_t>(p->L, 4);
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t b0 = p->L * c / n_chunks, b1 = p->L * (c + 1) / n_chunks;
+    cudaStream_t st = ws.streams[c & 1];
+    fmha_fwd_params pc = *p;
+    pc.L = b1 - b0;
+    const size_t oq = static_cast<size_t>(p->q_stride[0] * b0) * 2, ok_ = static_cast<size_t>(p->k_stride[0] * b0) * 2,
+                 ov = static_cast<size_t>(p->v_stride[0] * b0) * 2, oo = static_cast<size_t>(p->o_stride[0] * b0) * 2;
+    const size_t cq = static_cast<size_t>(p->q_stride[0] * pc.L) * 2, ck = static_cast<size_t>(p->k_stride[0] * pc.L) * 2,
+                 cv = static_cast<size_t>(p->v_stride[0] * pc.L) * 2, co = static_cast<size_t>(p->o_stride[0] * pc.L) * 2;
+    const size_t ol = static_cast<size_t>(b0 * p->h * p->N), cl = static_cast<size_t>(pc.L * p->h * p->N);
+    if ((e = cudaMemcpyAsync(dq + oq, static_cast<const char*>(q) + oq, cq, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dk + ok_, static_cast<const char*>(k) + ok_, ck, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dv + ov, static_cast<const char*>(v) + ov, cv, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync H2D");
+    s = fmha_fwd(&pc, dq + oq, dk + ok_, dv + ov, dO + oo, dl ? dl + ol : nullptr, st);
+    if (s != FMHA_OK) return s;
+    if ((e = cudaMemcpyAsync(static_cast<char*>(o) + oo, dO + oo, co, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync D2H");
+    if (lse && (e = cudaMemcpyAsync(lse + ol, dl + ol, cl * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync D2H lse");
+  }
+  g_last_launches = static_cast<int>(n_chunks);
+  if ((e = cudaStreamSynchronize(ws.streams[0])) != cudaSuccess ||
+      (e = cudaStreamSynchronize(ws.streams[1])) != cudaSuccess)
+    return cuda_fail(e, "kernel execution");
   return FMHA_OK;
 }
 
