@@ -104,11 +104,11 @@ int num_sms() {
   return n;
 }
 
-template <int D, bool BF16, int EMU = 0, bool ORDER = false>
+template <int D, bool BF16, int EMU = 0>
 fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st) {
   using Cfg = fmha_b200::FwdCfg<D>;
-  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU, ORDER>;
+  auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -126,7 +126,7 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
-  a.trace = trace_buffer(static_cast<size_t>(2 * a.n_kv_tiles * 8));
+  a.trace = trace_buffer(static_cast<size_t>(2 * a.n_kv_tiles * 16));
   const int grid = std::min(a.n_units, num_sms());
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
@@ -254,6 +254,8 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
   const bool bf = p->dtype == FMHA_BF16;
   switch (p->d) {
     case 64: {
+      // FMHA_TUNE_EMU64 selects the exp2 split for tuning runs (pairs of 16
+      // on the polynomial; default 4)
       static const int emu64 = [] {
         const char* e = std::getenv("FMHA_TUNE_EMU64");
         return e ? std::atoi(e) : 4;
@@ -261,18 +263,9 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       if (emu64 == 0)
         return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st);
-      if (emu64 == 10)  // tuning: softmax WGs take turns on MUFU, all-MUFU exp
-        return bf ? launch_d128<64, true, 0, true>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 0, true>(p, mq, mk, mv, mo, lse, st);
-      if (emu64 == 14)  // tuning: turns + 4/16 polynomial exp
-        return bf ? launch_d128<64, true, 4, true>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 4, true>(p, mq, mk, mv, mo, lse, st);
       if (emu64 == 6)
         return bf ? launch_d128<64, true, 6>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<64, false, 6>(p, mq, mk, mv, mo, lse, st);
-      if (emu64 == 8)
-        return bf ? launch_d128<64, true, 8>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 8>(p, mq, mk, mv, mo, lse, st);
       return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st)
                 : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
@@ -285,15 +278,9 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       if (emu == 0)
         return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
-      if (emu == 12)  // tuning: emu 4 with the softmax WGs taking turns on MUFU
-        return bf ? launch_d128<128, true, 4, true>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 4, true>(p, mq, mk, mv, mo, lse, st);
-      if (emu == 8)  // tuning: emu 0 with the softmax WGs taking turns on MUFU
-        return bf ? launch_d128<128, true, 0, true>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 0, true>(p, mq, mk, mv, mo, lse, st);
-      if (emu == 6)
-        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st);
+      if (emu == 2)
+        return bf ? launch_d128<128, true, 2>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 2>(p, mq, mk, mv, mo, lse, st);
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }

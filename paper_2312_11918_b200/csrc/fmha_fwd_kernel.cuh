@@ -50,12 +50,35 @@
 
 #include <cuda.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "sm100.cuh"
 #include "softmax_math.cuh"
 #include "tmem_ops.cuh"
 
+// Softmax publication variants (tuning knobs, fixed at build time)
+#ifndef FMHA_P_CHUNKS
+#define FMHA_P_CHUNKS 2  // P published in this many chunks of kv rows per tile
+#endif
+#ifndef FMHA_SPEC_MAX
+#define FMHA_SPEC_MAX 0  // exponentiate chunk 0 against the stale max while reducing the new one
+#endif
+#ifndef FMHA_MMA_SPIN
+#define FMHA_MMA_SPIN 0  // MMA warp spins (test_wait) on P instead of a suspending try_wait
+#endif
+#ifndef FMHA_DEFER_WAIT
+#define FMHA_DEFER_WAIT 0  // wait for chunk c's TMEM store only after chunk c+1's exps
+#endif
+
 namespace fmha_b200 {
+
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
 
 struct FwdArgs {
   void* o;                   // BSHD output (direct-store epilogue of the d=256 kernel)
@@ -71,15 +94,17 @@ struct FwdArgs {
 };
 
 // Debug timeline for the first unit of CTA 0: clock64 stamps written by one
-// thread per role.  trace[(q * n_kv + j) * 8 + k]:
-//   k=0 softmax woke (S ready)  1 S in registers  2 row max done
-//   3 P stored + arrived        4 MMA saw P ready  5 MMA issued PV+S
+// thread per role.  trace[(q * n_kv + j) * 16 + k]:
+//   k=0 softmax woke (S ready)  1 S in registers  8 row max done
+//   9 first-half exps done      2 first half published
+//   10 second-half exps done    3 second half published
+//   4 MMA saw P half 0   11 MMA saw P half 1   12 PV issued   5 S issued
 //   [6]/[7] of entry 0: kernel start / setup done; of the last tile:
 //   O ready / epilogue done.
 // Compiled in only with -DFMHA_TRACE_BUILD (tools/trace_timeline.py builds it).
 __device__ __forceinline__ void trace_stamp(const FwdArgs& a, bool on, int q, int j, int k) {
 #ifdef FMHA_TRACE_BUILD
-  if (on) a.trace[(q * a.n_kv_tiles + j) * 8 + k] = clock64();
+  if (on) a.trace[(q * a.n_kv_tiles + j) * 16 + k] = clock64();
 #endif
 }
 
@@ -96,12 +121,14 @@ struct FwdCfg {
   static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
   static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
-  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 14;
+  static constexpr int kPChunks = FMHA_P_CHUNKS;    // P published in chunks of kv rows
+  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 6;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
   static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
   static constexpr int kLoadWarp = 8;
   static constexpr int kMmaWarp = 9;
+  static constexpr int kStoreWarp = 10;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
@@ -116,7 +143,7 @@ __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int&
 }
 
 // kEmuPer16: of every 16 score pairs, how many take the FMA-pipe exp2.
-template <int D, bool kBF16, int kEmuPer16 = 0, bool kOrderExp = false>
+template <int D, bool kBF16, int kEmuPer16 = 0>
 __global__ void __launch_bounds__(384, 1)
     fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -136,13 +163,12 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* kv_full = bars + 2 * C::kQStages;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
-  uint64_t* p_full = s_full + 2;             // [2][2]: (tile q, kv half)
-  uint64_t* o_full = p_full + 4;             // [2]
+  uint64_t* p_full = s_full + 2;             // [2][kPChunks]: (tile q, chunk of kv rows)
+  uint64_t* o_full = p_full + 2 * C::kPChunks;  // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
   uint64_t* stage_free = o_empty + 2;        // O staging tile read by its TMA store
   uint64_t* stage_ready = stage_free + 1;    // O staging tile written by a softmax WG
-  uint64_t* exp_turn = stage_ready + 1;      // [2]: softmax WGs take turns on MUFU
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(exp_turn + 2);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -167,15 +193,12 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&s_full[q], 1);
-      mbar_init(&p_full[2 * q], 4);  // one arrival per softmax warp
-      mbar_init(&p_full[2 * q + 1], 4);
+      for (int c = 0; c < C::kPChunks; ++c) mbar_init(&p_full[q * C::kPChunks + c], 4);  // one per softmax warp
       mbar_init(&o_full[q], 1);
       mbar_init(&o_empty[q], 4);
     }
     mbar_init(stage_free, 1);
     mbar_init(stage_ready, 4);
-    mbar_init(&exp_turn[0], 4);
-    mbar_init(&exp_turn[1], 4);
     fence_mbar_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
@@ -277,24 +300,28 @@ __global__ void __launch_bounds__(384, 1)
       // O_q (+)= P_q V : M=128, N=D, K=128 kv rows in 8 steps of 16 rows.
       // A = P from TMEM (8 columns per step); B = V, MN-major (d contiguous):
       // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.  P arrives
-      // in two halves; each half's four MMAs start as soon as it is stored.
-      auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par) {
+      // in kPChunks chunks; each chunk's MMAs start as soon as it is stored.
+      auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par, bool trp, int jt) {
         const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
         const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
+        constexpr int kStepsPerChunk = 8 / C::kPChunks;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          mbar_wait(&p_full[2 * q + half], par);
+        for (int c = 0; c < C::kPChunks; ++c) {
+          if constexpr (FMHA_MMA_SPIN)
+            mbar_wait_spin(&p_full[q * C::kPChunks + c], par);
+          else
+            mbar_wait(&p_full[q * C::kPChunks + c], par);
+          if (c == C::kPChunks - 1) trace_stamp(args, trp, q, jt, 11);
           tc_fence_after();
 #pragma unroll
-          for (int kk = half * 4; kk < half * 4 + 4; ++kk) {
+          for (int kk = c * kStepsPerChunk; kk < (c + 1) * kStepsPerChunk; ++kk)
             mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
                          sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
                          (accumulate || kk > 0) ? 1u : 0u);
-          }
         }
       };
 
-      uint32_t it = 0;  // global K/V-tile counter (s_full / p_full parity)
+      uint32_t it = 0;  // global K/V-tile counter (p_full parity)
       int i = 0;
       for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
         const bool trm = tr && i == 0;
@@ -314,17 +341,15 @@ __global__ void __launch_bounds__(384, 1)
           const int vs = next_slot();
           ks = next_slot();
           const uint32_t par = it & 1;
-          mbar_wait(&p_full[0], par);
-          trace_stamp(args, trm, 0, j - 1, 4);
           if (j == 1) mbar_wait(&o_empty[0], ue);  // previous unit's epilogue drained O0
-          mma_pv(0, vs, j > 1, par);
+          mma_pv(0, vs, j > 1, par, trm, j - 1);
+          trace_stamp(args, trm, 0, j - 1, 12);
           mma_qk(0, ks);
           mma_commit_elect(&s_full[0]);
           trace_stamp(args, trm, 0, j - 1, 5);
-          mbar_wait(&p_full[2], par);
-          trace_stamp(args, trm, 1, j - 1, 4);
           if (j == 1) mbar_wait(&o_empty[1], ue);
-          mma_pv(1, vs, j > 1, par);
+          mma_pv(1, vs, j > 1, par, trm, j - 1);
+          trace_stamp(args, trm, 1, j - 1, 12);
           mma_qk(1, ks);
           mma_commit_elect(&s_full[1]);
           trace_stamp(args, trm, 1, j - 1, 5);
@@ -336,15 +361,15 @@ __global__ void __launch_bounds__(384, 1)
         const int vs = next_slot();
         const uint32_t par = it & 1;
         if (n_kv == 1) mbar_wait(&o_empty[0], ue);
-        mma_pv(0, vs, n_kv > 1, par);
+        mma_pv(0, vs, n_kv > 1, par, false, 0);
         mma_commit_elect(&o_full[0]);
         if (n_kv == 1) mbar_wait(&o_empty[1], ue);
-        mma_pv(1, vs, n_kv > 1, par);
+        mma_pv(1, vs, n_kv > 1, par, false, 0);
         mma_commit_elect(&o_full[1]);
         mma_commit_elect(&kv_empty[vs]);
         ++it;
       }
-    } else if (warp == 10) {
+    } else if (warp == C::kStoreWarp) {
       // ------------------------------------------------- O store warp --
       // Uses of the staging tile alternate WG0, WG1 per unit: use k = 2i+q.
       if (lane == 0) {
@@ -401,7 +426,7 @@ __global__ void __launch_bounds__(384, 1)
             if (c >= valid) s[c] = -INFINITY;
         }
         // Rescale O_q (TMEM) and the running sum by 2^((m - m_new) c); only
-        // called while O_q is quiescent (see the call sites).
+        // called while O_q is quiescent (S_q(j) observed => PV_q(j-1) done).
         auto rescale = [&](float m_new) {
           const float alpha = ex2_approx((m - m_new) * sl2);
           l *= alpha;
@@ -427,46 +452,85 @@ __global__ void __launch_bounds__(384, 1)
           return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         };
-        // publish half h of P (32 packed columns) to the MMA warp
-        auto publish = [&](const uint32_t(&p)[32], int half) {
-          tmem_st32x32b_x32(tS + half * 32, p);
+        // P chunk c = scores [c*kCW, (c+1)*kCW) -> kCW/2 packed columns of
+        // S_q's TMEM region (S is already in registers).
+        constexpr int kNC = C::kPChunks;
+        constexpr int kCW = 128 / kNC;
+        const bool masked = valid < C::kBN;
+        uint32_t pbuf[2][kCW / 2];
+        auto exp_chunk = [&](auto ci, float negv) -> float {
+          constexpr int c = decltype(ci)::value;
+          return masked ? exp_rowsum_pack<kBF16, c * kCW, kCW, 0>(s, sl2, negv, pbuf[c & 1])
+                        : exp_rowsum_pack<kBF16, c * kCW, kCW, kEmuPer16>(s, sl2, negv, pbuf[c & 1]);
+        };
+        auto store_chunk = [&](auto ci) {
+          constexpr int c = decltype(ci)::value;
+          if constexpr (kCW / 2 == 16)
+            tmem_st32x32b_x16(tS + c * (kCW / 2), pbuf[c & 1]);
+          else
+            tmem_st32x32b_x32(tS + c * (kCW / 2), pbuf[c & 1]);
+        };
+        auto arrive_chunk = [&](int c) {
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[2 * q + half]);
+          if (lane == 0) mbar_arrive(&p_full[q * kNC + c]);
         };
-        // The two WGs take turns on the exponential unit (WG0 tile t, WG1
-        // tile t, WG0 tile t+1, ...): the WG on the critical path never
-        // shares MUFU throughput, and each WG's non-exp work (TMEM load,
-        // publishing, waiting for the next S) hides under the other's turn.
-        if (kOrderExp) mbar_wait(&exp_turn[q], q ? (it & 1) : ((it & 1) ^ 1));
-        // Row max first (8 chains), then exponentiate against the running
-        // max.  Conditional rescale: keep the stale max unless some row of
-        // this warp grew by more than 8 (log2 units), i.e. P stays <= 256.
-        // S_q(j) observed => PV_q(j-1) complete, so O_q may be rescaled here.
-        {
-          const float m_new = fmaxf(row_max(), m);
-          if (__any_sync(0xffffffffu, (m_new - m) * sl2 > 8.0f)) {
+        float neg, rs;
+        if constexpr (FMHA_SPEC_MAX) {
+          // Speculative max: the first chunk is exponentiated against the
+          // running (stale) max while this tile's row max is reduced on the
+          // ALU pipe in parallel; recomputed only when the max moved.
+          neg = -m * sl2;
+          rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
+          const float mx = row_max();
+          trace_stamp(args, trq, q, j, 8);
+          if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
+            const float m_new = fmaxf(mx, m);
+            if (j == 0)
+              m = m_new;  // l = 0 and the first PV overwrites O
+            else
+              rescale(m_new);
+            neg = -m * sl2;
+            rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
+          }
+        } else {
+          // Conditional rescale (exact, since the final (m, Sigma) pair is
+          // consistent): a warp keeps its stale max unless some row's max
+          // grew by more than 8 in log2 units (P stays <= 256).
+          const float mx = row_max();
+          trace_stamp(args, trq, q, j, 8);
+          if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
+            const float m_new = fmaxf(mx, m);
             if (j == 0)
               m = m_new;  // l = 0 and the first PV overwrites O
             else
               rescale(m_new);
           }
+          neg = -m * sl2;
+          rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
         }
-        const float neg = -m * sl2;
-        uint32_t p[32];
-        const float rs_a = valid < C::kBN ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
-                                          : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
-        publish(p, 0);
-        trace_stamp(args, trq, q, j, 2);
-        const float rs_b = valid < C::kBN ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p)
-                                          : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p);
-        if (kOrderExp) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&exp_turn[q ^ 1]);
-        }
-        publish(p, 1);
-        l += rs_a + rs_b;
+        trace_stamp(args, trq, q, j, 9);
+        static_for<0, kNC>([&](auto ci) {
+          constexpr int c = decltype(ci)::value;
+          store_chunk(ci);
+          if constexpr (c + 1 < kNC) {
+            if constexpr (FMHA_DEFER_WAIT) {
+              // the store of chunk c is waited for after the next chunk's
+              // exponentials: the TMEM write latency leaves the critical path
+              rs += exp_chunk(std::integral_constant<int, c + 1>{}, neg);
+              arrive_chunk(c);
+            } else {
+              arrive_chunk(c);
+              rs += exp_chunk(std::integral_constant<int, c + 1>{}, neg);
+            }
+          } else {
+            trace_stamp(args, trq, q, j, 10);
+            arrive_chunk(c);
+          }
+          if constexpr (c == 0) trace_stamp(args, trq, q, j, 2);
+        });
+        l += rs;
         trace_stamp(args, trq, q, j, 3);
       }
 

@@ -79,6 +79,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Spin variant for a warp with nothing else to do that sits on the critical
+// path (the MMA issuer): non-blocking test_wait, no hardware suspend.
+__device__ __forceinline__ uint32_t mbar_test_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_test_wait(a, parity)) return;
+#ifndef FMHA_NO_WATCHDOG
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_test_wait(a, parity)) {
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
+#else
+  while (!mbar_test_wait(a, parity)) {
+  }
+#endif
+}
+
 // ----------------------------------------------------------------- TMA ---
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -1,5 +1,13 @@
-"""Debug: print the per-iteration timeline of CTA (0,0,0) (FMHA_TRACE=1).
-Run on a GPU:  FMHA_TRACE=1 python tools/trace_timeline.py [N] [d]"""
+"""Debug: per-K/V-tile timeline of CTA 0's first work unit (FMHA_TRACE=1).
+
+Run on a GPU (needs `make trace`):
+    FMHA_TRACE=1 python tools/trace_timeline.py [N] [d]
+
+Slots per (Q tile q, K/V tile j), see FwdArgs::trace in fmha_fwd_kernel.cuh:
+ softmax WG q: 0 woke (S ready)  1 S in registers  8 row max done  9 first-half exps
+               2 first half published  10 second-half exps  3 second half published
+ MMA warp:     4 saw P half 0  11 saw P half 1  12 PV issued  5 S(j+1) issued
+"""
 import ctypes as C
 import os
 import sys
@@ -20,32 +28,49 @@ q, k, v = (torch.randn(L, N, h, d, device="cuda").half() for _ in range(3))
 for _ in range(3):
     fm.fmha_fwd(q, k, v)
 torch.cuda.synchronize()
+S = 16
 n_kv = (N + 127) // 128
-buf = np.zeros(2 * n_kv * 8, np.uint64)
+buf = np.zeros(2 * n_kv * S, np.uint64)
 fm.lib().fmha_debug_trace_copy(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
-t = buf.reshape(2, n_kv, 8).astype(np.int64)
-t0 = t[0, 0, 6]
-t = np.where(t > 0, t - t0, -1)
-names = ["wake", "ld", "max", "P+arrive", "mma_sawP", "mma_issued"]
-print("q j | " + " ".join(f"{n:>10s}" for n in names) + " | ld  max  exp  P->mma  issue")
-for j in range(min(n_kv, 12)):
-    for qq in range(2):
-        r = t[qq, j]
-        print(f"{qq} {j:2d} | " + " ".join(f"{x:10d}" for x in r[:6]) +
-              f" | {r[1]-r[0]:4d} {r[2]-r[1]:4d} {r[3]-r[2]:5d} {r[4]-r[3]:6d} {r[5]-r[4]:5d}")
-if n_kv > 3:
-    per = np.diff(t[0, 2:n_kv - 1, 0])
-    print("steady-state period per K/V tile (clk): median", int(np.median(per)), "min", int(per.min()))
-if n_kv <= 3:
-    sys.exit(0)
-d_ld = np.median(t[:, 2:-1, 1] - t[:, 2:-1, 0]); d_max = np.median(t[:, 2:-1, 2] - t[:, 2:-1, 1])
-d_exp = np.median(t[:, 2:-1, 3] - t[:, 2:-1, 2]); d_p2m = np.median(t[:, 2:-2, 4] - t[:, 2:-2, 3])
-d_iss = np.median(t[:, 2:-2, 5] - t[:, 2:-2, 4])
-d_tc = np.median(t[:, 3:-1, 0] - t[:, 2:-2, 5])
-print(f"median: ldtm {d_ld:.0f}  max {d_max:.0f}  exp+store+arrive {d_exp:.0f}  P->MMA wake {d_p2m:.0f}  "
-      f"MMA issue {d_iss:.0f}  issue->S ready {d_tc:.0f}")
+t = buf.reshape(2, n_kv, S).astype(np.int64)
+start, setup = t[0, 0, 6], t[0, 0, 7]
+t = np.where(t > 0, t - start, -1)
 
-print(f"kernel start -> setup done {t[0,0,7]}  first S ready (q0) {t[0,0,0]}  (q1) {t[1,0,0]}")
+SEG = [  # (name, from slot, to slot, same j?)
+    ("S ready->in regs", 0, 1), ("row max", 1, 8), ("exp half0", 8, 9), ("publish0", 9, 2),
+    ("exp half1", 2, 10), ("publish1", 10, 3), ("P1 arrive->MMA saw", 3, 11), ("PV issue", 11, 12),
+    ("S issue", 12, 5),
+]
+print(f"N={N} d={d} n_kv={n_kv}  setup {setup - start} clk, first S ready q0 {t[0,0,0]} q1 {t[1,0,0]}")
+lo, hi = 2, n_kv - 2
+for name, a, b in SEG:
+    vals = t[:, lo:hi, b] - t[:, lo:hi, a]
+    print(f"  {name:22s} median q0 {np.median(vals[0]):6.0f}  q1 {np.median(vals[1]):6.0f}")
+issue_to_next = t[:, lo + 1:hi + 1, 0] - t[:, lo:hi, 5]
+print(f"  {'S issued->next wake':22s} median q0 {np.median(issue_to_next[0]):6.0f}  q1 {np.median(issue_to_next[1]):6.0f}")
+per = np.diff(t[0, lo:hi, 0])
+print(f"steady-state period per K/V tile: median {np.median(per):.0f} clk, min {per.min()}")
+# overlap of the two softmax WGs' busy intervals [in regs, published]
+busy0 = [(t[0, j, 1], t[0, j, 3]) for j in range(lo, hi)]
+busy1 = [(t[1, j, 1], t[1, j, 3]) for j in range(lo, hi)]
+ov = 0
+for a0, b0 in busy0:
+    for a1, b1 in busy1:
+        ov += max(0, min(b0, b1) - max(a0, a1))
+tot = t[0, hi - 1, 3] - t[0, lo, 1]
+print(f"softmax WG busy fraction: q0 {sum(b - a for a, b in busy0) / tot:.2f}  q1 {sum(b - a for a, b in busy1) / tot:.2f}  "
+      f"overlapped {ov / tot:.2f}")
+print("\nraw timeline, tiles 4..6 (clk since kernel start):")
+ev = []
+names = {0: "wake", 1: "ld", 8: "max", 9: "exp0", 2: "pub0", 10: "exp1", 3: "pub1", 4: "mma saw P0", 11: "mma saw P1",
+         12: "PV issued", 5: "S issued"}
+for j in range(4, min(7, n_kv)):
+    for qq in range(2):
+        for sl, nm in names.items():
+            if t[qq, j, sl] >= 0:
+                ev.append((t[qq, j, sl], f"q{qq} j{j} {nm}"))
+for x, nm in sorted(ev):
+    print(f"  {x:8d}  {nm}")
 for qq in range(2):
-    print(f"q{qq}: last P arrive {t[qq,-1,3]}  O ready {t[qq,-1,6]}  epilogue done {t[qq,-1,7]}  "
-          f"(mainloop {t[qq,-1,3]-t[qq,0,0]} clk for {n_kv} tiles = {(t[qq,-1,3]-t[qq,0,0])/n_kv:.0f}/tile)")
+    print(f"q{qq}: last P {t[qq,-1,3]}  O ready {t[qq,-1,6]}  epilogue done {t[qq,-1,7]}  "
+          f"mainloop {(t[qq,-1,3]-t[qq,0,0])/n_kv:.0f} clk/tile")
