@@ -163,7 +163,16 @@ fmha_status launch_d256(const fmha_fwd_params* p, const CUtensorMap& mq, const C
             static_cast<unsigned>(p->L));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    return fail(FMHA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e) + " (regs " +
+                                   std::to_string(fa.numRegs) + ", max threads " +
+                                   std::to_string(fa.maxThreadsPerBlock) + ", local " +
+                                   std::to_string(fa.localSizeBytes) + " B, launch " +
+                                   std::to_string(Cfg::kThreads) + " threads, smem " +
+                                   std::to_string(Cfg::kSmemAlloc) + ")");
+  }
   g_last_launches = 1;
   return FMHA_OK;
 }

@@ -32,7 +32,8 @@ S = 16
 n_kv = (N + 127) // 128
 buf = np.zeros(2 * n_kv * S, np.uint64)
 fm.lib().fmha_debug_trace_copy(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
-t = buf.reshape(2, n_kv, S).astype(np.int64)
+full = buf.reshape(-1, n_kv, S).astype(np.int64)
+t = full[:2]
 start, setup = t[0, 0, 6], t[0, 0, 7]
 t = np.where(t > 0, t - start, -1)
 
@@ -74,3 +75,4 @@ for x, nm in sorted(ev):
 for qq in range(2):
     print(f"q{qq}: last P {t[qq,-1,3]}  O ready {t[qq,-1,6]}  epilogue done {t[qq,-1,7]}  "
           f"mainloop {(t[qq,-1,3]-t[qq,0,0])/n_kv:.0f} clk/tile")
+
