@@ -359,9 +359,30 @@ def measure_e2e(fm, q, k, v, cfg, args, world, dev):
     dt = float(tt.item())
     bi = 3 * hq.numel() * hq.element_size()
     bo = ho.numel() * ho.element_size() + hl.numel() * 4
+    # the e2e roofline: host->device copy of the inputs at this box's measured
+    # pinned H2D rate (the D2H of O/LSE overlaps it; PCIe is full duplex)
+    pcie = measure_h2d_gbps(dev)
+    bound_ms = bi / (pcie * 1e9) * 1e3
     return {"value": world * flops(L, N, h, d) * steps / dt / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": steps,
-            "api": "fmha_fwd_host (C ABI, pinned host fp16 buffers)"}
+            "ms_per_step": dt / steps * 1e3,
+            "roofline": {"bound": "pcie_h2d", "h2d_GBps_measured": pcie, "bound_ms": bound_ms,
+                         "frac": bound_ms / (dt / steps * 1e3)},
+            "api": "fmha_fwd_host (C ABI, pinned host 16-bit buffers; 3-stream H2D/kernel/D2H pipeline)"}
+
+
+def measure_h2d_gbps(dev, mb=128, reps=3):
+    """Pinned host->device copy rate on this box (GB/s), contiguous."""
+    import torch
+    hbuf = torch.empty(mb << 20, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
+    dbuf.copy_(hbuf, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        dbuf.copy_(hbuf, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    return reps * (mb << 20) / (time.perf_counter() - t0) / 1e9
 
 
 def main():

@@ -10,6 +10,8 @@
 
 #include <cstdio>
 
+#include <cuda_fp16.h>
+
 #include "softmax_math.cuh"
 
 using namespace fmha_b200;
@@ -55,6 +57,49 @@ __device__ __forceinline__ float exp_sum_scalar(const float (&s)[128], float c, 
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
 
+// f16 formulation: S pair -> f16x2 (F2FP) -> x = s*c - m*c in f16x2 (HFMA2)
+// -> ex2.approx.f16x2 (MUFU) gives packed P directly; row sum as f16x2 adds
+// (HADD2) into 4 accumulators, widened to f32 once per chunk.
+__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_add(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_ex2(uint32_t a) {
+  uint32_t d;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+template <int EMU, int kOff, int kCols>
+__device__ __forceinline__ float exp_sum_h16(const float (&s)[128], float c, float nm, uint32_t (&p)[kCols / 2]) {
+  const uint32_t c2 = pack2<false>(c, c), nm2 = pack2<false>(nm, nm);
+  uint32_t a[4] = {0u, 0u, 0u, 0u};
+  float fs = 0.f;
+#pragma unroll
+  for (int i = 0; i < kCols / 2; ++i) {
+    if ((i & 15) < EMU) {  // fp32 polynomial path
+      const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), f2_pack(c, c), f2_pack(nm, nm));
+      const uint64_t e = exp2_poly_x2(x);
+      float e0, e1;
+      f2_unpack(e, e0, e1);
+      fs += e0 + e1;
+      p[i] = pack2<false>(e0, e1);
+    } else {
+      const uint32_t h = pack2<false>(s[kOff + 2 * i], s[kOff + 2 * i + 1]);
+      p[i] = h2_ex2(h2_fma(h, c2, nm2));
+      a[i & 3] = h2_add(a[i & 3], p[i]);
+    }
+  }
+  const uint32_t t = h2_add(h2_add(a[0], a[1]), h2_add(a[2], a[3]));
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&t));
+  return f.x + f.y + fs;
+}
+
 __device__ __forceinline__ float row_max128(const float (&s)[128]) {
   float mx[8];
 #pragma unroll
@@ -94,6 +139,8 @@ __global__ void __launch_bounds__(256, 1) probe(const float* in, uint32_t* out, 
     uint32_t* dst = sh_p + threadIdx.x * 36;
     if (MODE == 0) {
       sum += exp_rowsum_pack<false, 0, 64, EMU>(s, c, nm, p);
+    } else if (MODE == 5) {
+      sum += exp_sum_h16<EMU, 0, 64>(s, c, nm, p);
     } else {
       sum += exp_sum_scalar<EMU, MODE == 2 ? 3 : 4, 0, 64>(s, c, nm, p);
     }
@@ -101,6 +148,8 @@ __global__ void __launch_bounds__(256, 1) probe(const float* in, uint32_t* out, 
     for (int i = 0; i < 32; i += 4) st_shared_v4(dst + i, p[i], p[i + 1], p[i + 2], p[i + 3]);
     if (MODE == 0) {
       sum += exp_rowsum_pack<false, 64, 64, EMU>(s, c, nm, p);
+    } else if (MODE == 5) {
+      sum += exp_sum_h16<EMU, 64, 64>(s, c, nm, p);
     } else {
       sum += exp_sum_scalar<EMU, MODE == 2 ? 3 : 4, 64, 64>(s, c, nm, p);
     }
@@ -137,16 +186,12 @@ void run(int threads, const char* name) {
 
 int main() {
   for (int t : {128, 256}) {
-    run<0, 0>(t, "packed (16ths)");
-    run<0, 4>(t, "packed (16ths)");
-    run<1, 0>(t, "scalar deg4 (8ths)");
-    run<1, 1>(t, "scalar deg4 (8ths)");
-    run<1, 2>(t, "scalar deg4 (8ths)");
-    run<1, 3>(t, "scalar deg4 (8ths)");
-    run<2, 1>(t, "scalar deg3 (8ths)");
-    run<2, 2>(t, "scalar deg3 (8ths)");
-    run<2, 3>(t, "scalar deg3 (8ths)");
-    run<2, 4>(t, "scalar deg3 (8ths)");
+    run<0, 0>(t, "packed f32 (16ths)");
+    run<0, 4>(t, "packed f32 (16ths)");
+    run<5, 0>(t, "f16x2 mufu (16ths)");
+    run<5, 2>(t, "f16x2 + f32 poly (16ths)");
+    run<5, 4>(t, "f16x2 + f32 poly (16ths)");
+    run<5, 6>(t, "f16x2 + f32 poly (16ths)");
   }
   return 0;
 }
