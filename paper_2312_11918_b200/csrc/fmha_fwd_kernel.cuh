@@ -63,6 +63,9 @@
 #ifndef FMHA_SPEC_MAX
 #define FMHA_SPEC_MAX 0  // exponentiate chunk 0 against the stale max while reducing the new one
 #endif
+#ifndef FMHA_MASKED_EXACT
+#define FMHA_MASKED_EXACT 1  // padded (masked) tiles take an all-MUFU copy of the exp code
+#endif
 #ifndef FMHA_MMA_SPIN
 #define FMHA_MMA_SPIN 0  // MMA warp spins (test_wait) on P instead of a suspending try_wait
 #endif
@@ -460,8 +463,13 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t pbuf[2][kCW / 2];
         auto exp_chunk = [&](auto ci, float negv) -> float {
           constexpr int c = decltype(ci)::value;
+#if FMHA_MASKED_EXACT
           return masked ? exp_rowsum_pack<kBF16, c * kCW, kCW, 0>(s, sl2, negv, pbuf[c & 1])
                         : exp_rowsum_pack<kBF16, c * kCW, kCW, kEmuPer16>(s, sl2, negv, pbuf[c & 1]);
+#else
+          (void)masked;
+          return exp_rowsum_pack<kBF16, c * kCW, kCW, kEmuPer16>(s, sl2, negv, pbuf[c & 1]);
+#endif
         };
         auto store_chunk = [&](auto ci) {
           constexpr int c = decltype(ci)::value;
@@ -532,6 +540,10 @@ __global__ void __launch_bounds__(384, 1)
         });
         l += rs;
         trace_stamp(args, trq, q, j, 3);
+#ifdef FMHA_TRACE_BUILD
+        // per-warp completion times of the first unit: trace[(2*n_kv + j)*16 + warp]
+        if (tr && i == 0 && lane == 0) args.trace[(2 * n_kv + j) * 16 + warp] = clock64();
+#endif
       }
 
       // ----------------------------------------------------- epilogue --

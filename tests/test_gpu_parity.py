@@ -201,3 +201,28 @@ def test_launch_count():
     q = torch.randn(1, 256, 1, 64, device="cuda").half()
     fm.fmha_fwd(q, q, q)
     assert fm.launch_count() == 1
+
+
+@pytest.mark.parametrize("L,N,h,d,dt", [
+    (2, 4096, 16, 128, "f16"),   # 1 batch per input chunk, O/LSE returned in 4 head groups (2-D copies)
+    (8, 512, 8, 64, "bf16"),     # several batches per input chunk
+    (3, 2048, 6, 256, "f16"),    # d=256 kernel behind the pipeline
+])
+def test_host_pipeline_bitwise_equals_device_path(L, N, h, d, dt):
+    """fmha_fwd_host splits the problem into (batch, head-group) chunks over
+    three streams; every chunk is an independent sub-problem, so the result
+    must equal the single-launch device path bit for bit."""
+    import torch
+    import paper_2312_11918_b200 as fm
+    td = torch.bfloat16 if dt == "bf16" else torch.float16
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = (torch.randn((L, N, h, d), generator=g, device="cuda").to(td) for _ in range(3))
+    o_dev, lse_dev = fm.fmha_fwd(q, k, v)
+    torch.cuda.synchronize()
+    hq, hk, hv = (x.cpu().view(torch.int16).numpy() for x in (q, k, v))
+    ho = np.empty_like(hq)
+    hl = np.empty((L, h, N), np.float32)
+    fm.fmha_fwd_host(hq, hk, hv, ho, hl, dtype=fm.BF16 if dt == "bf16" else fm.F16)
+    assert fm.launch_count() >= 1
+    assert np.array_equal(ho, o_dev.cpu().view(torch.int16).numpy())
+    assert np.array_equal(hl, lse_dev.cpu().numpy())

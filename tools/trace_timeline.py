@@ -30,10 +30,11 @@ for _ in range(3):
 torch.cuda.synchronize()
 S = 16
 n_kv = (N + 127) // 128
-buf = np.zeros(2 * n_kv * S, np.uint64)
+buf = np.zeros(3 * n_kv * S, np.uint64)
 fm.lib().fmha_debug_trace_copy(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
 full = buf.reshape(-1, n_kv, S).astype(np.int64)
 t = full[:2]
+warp_t = full[2].astype(np.int64)
 start, setup = t[0, 0, 6], t[0, 0, 7]
 t = np.where(t > 0, t - start, -1)
 
@@ -76,3 +77,11 @@ for qq in range(2):
     print(f"q{qq}: last P {t[qq,-1,3]}  O ready {t[qq,-1,6]}  epilogue done {t[qq,-1,7]}  "
           f"mainloop {(t[qq,-1,3]-t[qq,0,0])/n_kv:.0f} clk/tile")
 
+
+w = warp_t - start
+print("\nper-warp P-complete time minus the tile's earliest (warp w: tile w//4, SM sub-partition w%4), tiles 4..9:")
+for j in range(4, min(10, n_kv)):
+    for qq in range(2):
+        ws = [4 * qq + x for x in range(4)]
+        base = min(w[j, x] for x in ws)
+        print(f"  j{j} q{qq}: " + " ".join(f"w{x}:{w[j, x] - base:5d}" for x in ws))
