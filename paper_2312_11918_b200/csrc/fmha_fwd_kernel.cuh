@@ -34,7 +34,9 @@
 // preceding PV_q(j-1) has completed too: the WG may rescale O_q in TMEM
 // without any further barrier, and P_q(j) may overwrite S_q(j)'s columns.
 // P is published in two halves (kv rows 0-63 / 64-127) so GEMM-II on the
-// first half overlaps the exponentials of the second.
+// first half overlaps the end of the softmax; the TMEM store of half 0 is
+// waited for (tcgen05.wait::st, ~200 clk) only after half 1's exponentials
+// are computed, so the warp never idles on it.
 //
 // Across units: the producer loads the next unit's Q as soon as the last
 // S GEMMs of the current unit have completed (`q_empty`), the MMA warp
@@ -70,7 +72,7 @@
 #define FMHA_MMA_SPIN 0  // MMA warp spins (test_wait) on P instead of a suspending try_wait
 #endif
 #ifndef FMHA_DEFER_WAIT
-#define FMHA_DEFER_WAIT 0  // wait for chunk c's TMEM store only after chunk c+1's exps
+#define FMHA_DEFER_WAIT 1  // wait for chunk c's TMEM store only after chunk c+1's exps
 #endif
 
 namespace fmha_b200 {
