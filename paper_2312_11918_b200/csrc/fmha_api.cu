@@ -327,6 +327,9 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       if (emu64 == 6)
         return bf ? launch_d128<64, true, 6>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<64, false, 6>(p, mq, mk, mv, mo, lse, st);
+      if (emu64 == 8)
+        return bf ? launch_d128<64, true, 8>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<64, false, 8>(p, mq, mk, mv, mo, lse, st);
       return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st)
                 : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
@@ -342,6 +345,12 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       if (emu == 2)
         return bf ? launch_d128<128, true, 2>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<128, false, 2>(p, mq, mk, mv, mo, lse, st);
+      if (emu == 6)
+        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st);
+      if (emu == 8)
+        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st)
+                  : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st);
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }

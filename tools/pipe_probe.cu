@@ -186,12 +186,12 @@ void run(int threads, const char* name) {
 
 int main() {
   for (int t : {128, 256}) {
-    run<0, 0>(t, "packed f32 (16ths)");
-    run<0, 4>(t, "packed f32 (16ths)");
-    run<5, 0>(t, "f16x2 mufu (16ths)");
-    run<5, 2>(t, "f16x2 + f32 poly (16ths)");
-    run<5, 4>(t, "f16x2 + f32 poly (16ths)");
-    run<5, 6>(t, "f16x2 + f32 poly (16ths)");
+    run<0, 0>(t, "packed f32 deg3 (16ths)");
+    run<0, 1>(t, "packed f32 deg3 (16ths)");
+    run<0, 2>(t, "packed f32 deg3 (16ths)");
+    run<0, 3>(t, "packed f32 deg3 (16ths)");
+    run<0, 4>(t, "packed f32 deg3 (16ths)");
+    run<0, 6>(t, "packed f32 deg3 (16ths)");
   }
   return 0;
 }
