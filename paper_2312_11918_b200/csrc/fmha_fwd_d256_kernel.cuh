@@ -2,15 +2,23 @@
 //
 // Same contract as fmha_fwd_kernel.cuh (fmhasim::fmha_forward,
 // /root/reference/proj/src/attention.cpp:153-173) but shaped for d = 256,
-// where the O accumulator alone needs 256 TMEM columns and a 128 x 256
-// 16-bit K or V tile is 64 KB:
+// where the O accumulator alone needs 256 TMEM columns and a K or V tile is
+// kBN x 512 B:
 //
-//   CTA = one (b, head) and ONE 128-row Q tile; K/V tiles of 64 rows.
-//   TMEM: S buffers A [0,64) and B [64,128) (double-buffered so the tensor
-//         core computes S(j+1) while softmax works on S(j)); O [256,512).
-//         P(j) (16-bit) aliases the first 32 columns of its S buffer.
-//   smem: Q 64 KB + 4-slot K/V ring of 32 KB = 192 KB.
+//   CTA = one (b, head) and ONE 128-row Q tile; K/V tiles of kBN rows.
+//   TMEM: S buffers A [0,kBN) and B [kBN,2kBN) (double-buffered, so the
+//         tensor core computes S(j+1) while softmax works on S(j));
+//         O [256,512).  P(j) (16-bit) aliases the first kBN/2 columns of its
+//         S buffer.
+//   smem: Q 64 KB + K/V ring of 128 KB (4 x 32 KB at kBN = 64, 2 x 64 KB at
+//         kBN = 128), loaded in the MMA warp's consumption order
+//         K0 K1 | V0 K2 | V1 K3 | ... so a 2-slot ring still gives every
+//         load one S or PV GEMM (~1k clk) of lead time.
 //   warps 0-3 softmax (thread per row), warp 4 TMA producer, warp 5 MMA.
+//
+// kBN = 128 (default): S GEMMs are M128 N128 (8 KB of shared memory per
+// 64-clk MMA, the shared-memory rate); at kBN = 64 the N=64 S GEMMs are
+// shared-memory bound at 48 clk per 32-clk MMA (tools/mma_probe.cu).
 //
 // MMA order: S(0) S(1) | PV(0) S(2) | PV(1) S(3) | ...  PV(j) is committed to
 // `pv_done` so the softmax WG can wait for O(j-1) before a conditional
@@ -23,18 +31,21 @@
 
 #include "fmha_fwd_kernel.cuh"
 #include "sm100.cuh"
+#include "softmax_math.cuh"
 #include "tmem_ops.cuh"
 
 namespace fmha_b200 {
 
+template <int kBN_>
 struct FwdCfgD256 {
   static constexpr int D = 256;
   static constexpr int kBM = 128;
-  static constexpr int kBN = 64;
+  static constexpr int kBN = kBN_;
+  static_assert(kBN == 64 || kBN == 128, "K/V step of 64 or 128 rows");
   static constexpr int kChunks = 4;
   static constexpr int kQTileBytes = kBM * D * 2;    // 64 KB
-  static constexpr int kKVTileBytes = kBN * D * 2;   // 32 KB
-  static constexpr int kStages = 4;
+  static constexpr int kKVTileBytes = kBN * D * 2;   // 32 / 64 KB
+  static constexpr int kStages = kBN == 64 ? 4 : 2;
   static constexpr int kSmemRing = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 2;
   static constexpr int kSmemBytes = kQTileBytes + kSmemRing + kNumBars * 8 + 16;
@@ -42,17 +53,18 @@ struct FwdCfgD256 {
   static constexpr int kThreads = 192;
   static constexpr int kLoadWarp = 4;
   static constexpr int kMmaWarp = 5;
-  __host__ __device__ static constexpr uint32_t col_s(int buf) { return buf ? 64u : 0u; }
+  __host__ __device__ static constexpr uint32_t col_s(int buf) { return buf ? static_cast<uint32_t>(kBN) : 0u; }
   static constexpr uint32_t kColO = 256;
   static constexpr uint32_t kTmemCols = 512;
+  static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16>
+template <bool kBF16, int kBN = 128, int kEmuPer16 = 4>
 __global__ void __launch_bounds__(192, 1)
     fmha_fwd_d256_kernel(const __grid_constant__ CUtensorMap tmQ,
                          const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
-  using C = FwdCfgD256;
+  using C = FwdCfgD256<kBN>;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -107,17 +119,26 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int c = 0; c < C::kChunks; ++c)
         tma_load_4d_hint(&tmQ, bar_q, sQ + c * C::kBM * 128, c * 64, head, qrow0, b, once);
-      // item t: K_{t/2} (t even) or V_{t/2} (t odd); slot t % S, use (t / S)
-      for (int t = 0; t < 2 * n_kv; ++t) {
-        const int slot = t % C::kStages;
-        const uint32_t use = static_cast<uint32_t>(t / C::kStages);
-        mbar_wait(&kv_empty[slot], (use & 1) ^ 1);
+      int slot = 0;
+      uint32_t phase = 0;
+      auto load = [&](const CUtensorMap* map, int step) {
+        mbar_wait(&kv_empty[slot], phase ^ 1);
         mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
         uint8_t* dst = sRing + slot * C::kKVTileBytes;
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_4d_hint((t & 1) ? &tmV : &tmK, &kv_full[slot], dst + c * C::kBN * 128, c * 64,
-                           head, (t >> 1) * C::kBN, b, keep);
+          tma_load_4d_hint(map, &kv_full[slot], dst + c * C::kBN * 128, c * 64, head, step * C::kBN, b, keep);
+        if (++slot == C::kStages) {
+          slot = 0;
+          phase ^= 1;
+        }
+      };
+      // consumption order of the MMA warp: K0 K1 | V0 K2 | V1 K3 | ...
+      load(&tmK, 0);
+      if (n_kv > 1) load(&tmK, 1);
+      for (int j = 0; j < n_kv; ++j) {
+        load(&tmV, j);
+        if (j + 2 < n_kv) load(&tmK, j + 2);
       }
     }
   } else if (warp == C::kMmaWarp) {
@@ -126,10 +147,16 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t kIdescPV = idesc_f16(kBF16, C::kBM, D, false, true);
       const uint32_t sQ_addr = smem_u32(sQ);
       const uint32_t ring_addr = smem_u32(sRing);
-      auto wait_item = [&](int t) -> int {
-        const int slot = t % C::kStages;
-        mbar_wait(&kv_full[slot], static_cast<uint32_t>(t / C::kStages) & 1);
-        return slot;
+      int slot = 0;
+      uint32_t phase = 0;
+      auto next_slot = [&]() -> int {
+        const int s = slot;
+        mbar_wait(&kv_full[s], phase);
+        if (++slot == C::kStages) {
+          slot = 0;
+          phase ^= 1;
+        }
+        return s;
       };
       auto mma_qk = [&](int buf, int kslot) {
         const uint32_t b0 = ring_addr + kslot * C::kKVTileBytes;
@@ -138,7 +165,7 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
           const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
           mma_ss_elect(tmem + C::col_s(buf), sdesc_sw128(sQ_addr + off_a, 16, 1024),
-                 sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+                       sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
       auto mma_pv = [&](int buf, int vslot, bool accumulate) {
@@ -146,13 +173,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int kk = 0; kk < C::kBN / 16; ++kk)
           mma_ts_elect(tmem + C::kColO, tmem + C::col_s(buf) + kk * 8,
-                 sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
-                 (accumulate || kk > 0) ? 1u : 0u);
+                       sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
+                       (accumulate || kk > 0) ? 1u : 0u);
       };
 
       mbar_wait(bar_q, 0);
       for (int t = 0; t < 2 && t < n_kv; ++t) {
-        const int ks = wait_item(2 * t);
+        const int ks = next_slot();
         tc_fence_after();
         mma_qk(t, ks);
         mma_commit_elect(&s_full[t]);
@@ -160,14 +187,14 @@ __global__ void __launch_bounds__(192, 1)
       }
       for (int j = 0; j < n_kv; ++j) {
         const int buf = j & 1;
-        const int vs = wait_item(2 * j + 1);
+        const int vs = next_slot();
         mbar_wait(&p_full[buf], static_cast<uint32_t>(j >> 1) & 1);
         tc_fence_after();
         mma_pv(buf, vs, j > 0);
         mma_commit_elect(pv_done);
         mma_commit_elect(&kv_empty[vs]);
         if (j + 2 < n_kv) {
-          const int ks = wait_item(2 * (j + 2));
+          const int ks = next_slot();
           tc_fence_after();
           mma_qk(buf, ks);
           mma_commit_elect(&s_full[buf]);
@@ -189,28 +216,31 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tS = tmem + lane_off + C::col_s(buf);
       mbar_wait(&s_full[buf], static_cast<uint32_t>(j >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[64];
-      tmem_ld32x32b_x64(tS, sr);
-      float s[64];
+      uint32_t sr[C::kBN];
+      if constexpr (C::kBN == 128)
+        tmem_ld32x32b_x128(tS, sr);
+      else
+        tmem_ld32x32b_x64(tS, sr);
+      float s[C::kBN];
 #pragma unroll
-      for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+      for (int c = 0; c < C::kBN; ++c) s[c] = __uint_as_float(sr[c]);
       const int valid = N - j * C::kBN;
       if (valid < C::kBN) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
+        for (int c = 0; c < C::kBN; ++c)
           if (c >= valid) s[c] = -INFINITY;
       }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+      float mx[8];
 #pragma unroll
-      for (int c = 4; c < 64; c += 4) {
-        mx0 = fmaxf(mx0, s[c]);
-        mx1 = fmaxf(mx1, s[c + 1]);
-        mx2 = fmaxf(mx2, s[c + 2]);
-        mx3 = fmaxf(mx3, s[c + 3]);
-      }
-      const float m_new = fmaxf(m, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
-      const bool need = (m_new - m) * sl2 > 8.0f;
-      if (__any_sync(0xffffffffu, need)) {
+      for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
+#pragma unroll
+      for (int c = 16; c < C::kBN; c += 16)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
+      const float m_new = fmaxf(m, fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))));
+      // conditional rescale (exact: the final (m, Sigma) pair is consistent)
+      if (__any_sync(0xffffffffu, (m_new - m) * sl2 > 8.0f)) {
         const float alpha = ex2_approx((m - m_new) * sl2);
         l *= alpha;
         if (j > 0) {
@@ -228,23 +258,24 @@ __global__ void __launch_bounds__(192, 1)
         m = m_new;
       }
       const float neg = -m * sl2;
-      float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
-      uint32_t p[32];
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const float e0 = ex2_approx(fmaf(s[2 * i], sl2, neg));
-        const float e1 = ex2_approx(fmaf(s[2 * i + 1], sl2, neg));
-        const float e2 = ex2_approx(fmaf(s[2 * i + 2], sl2, neg));
-        const float e3 = ex2_approx(fmaf(s[2 * i + 3], sl2, neg));
-        rs0 += e0;
-        rs1 += e1;
-        rs2 += e2;
-        rs3 += e3;
-        p[i] = pack2<kBF16>(e0, e1);
-        p[i + 1] = pack2<kBF16>(e2, e3);
+      const bool masked = valid < C::kBN;
+      uint32_t p[C::kBN / 2];
+      float rs;
+      if constexpr (C::kBN == 128) {
+        uint32_t p0[32], p1[32];
+        rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
+                    : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+        tmem_st32x32b_x32(tS, p0);
+        rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
+                     : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        tmem_st32x32b_x32(tS + 32, p1);
+        (void)p;
+      } else {
+        rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p)
+                    : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p);
+        tmem_st32x32b_x32(tS, p);
       }
-      tmem_st32x32b_x32(tS, p);
-      l += (rs0 + rs1) + (rs2 + rs3);
+      l += rs;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[buf]);
