@@ -18,7 +18,7 @@
 
 #include "../../include/fmha/fmha.h"
 #include "fmha_errors.hpp"
-#include "fmha_fwd_d256_kernel.cuh"
+#include "fmha_fwd_st_kernel.cuh"
 #include "fmha_fwd_kernel.cuh"
 
 namespace {
@@ -144,11 +144,11 @@ int d256_bn() {
   return bn;
 }
 
-template <bool BF16, int BN>
-fmha_status launch_d256(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
-                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
-  using Cfg = fmha_b200::FwdCfgD256<BN>;
-  auto kern = fmha_b200::fmha_fwd_d256_kernel<BF16, BN>;
+template <int D, bool BF16, int BN>
+fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
+                      const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+  using Cfg = fmha_b200::FwdCfgST<D, BN>;
+  auto kern = fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -365,8 +365,8 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     }
     default:
       if (d256_bn() == 64)
-        return bf ? launch_d256<true, 64>(p, mq, mk, mv, o, lse, st) : launch_d256<false, 64>(p, mq, mk, mv, o, lse, st);
-      return bf ? launch_d256<true, 128>(p, mq, mk, mv, o, lse, st) : launch_d256<false, 128>(p, mq, mk, mv, o, lse, st);
+        return bf ? launch_st<256, true, 64>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 64>(p, mq, mk, mv, o, lse, st);
+      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st);
   }
 }
 

@@ -1,4 +1,5 @@
-// fmha_fwd_d256_kernel.cuh -- FMHA forward for head dim 256 on sm_100a.
+// fmha_fwd_st_kernel.cuh -- single-Q-tile FMHA forward with double-buffered S
+// (used for head dim 256; D = 64 / 128 instantiations measured).
 //
 // Same contract as fmha_fwd_kernel.cuh (fmhasim::fmha_forward,
 // /root/reference/proj/src/attention.cpp:153-173) but shaped for d = 256,
@@ -36,16 +37,28 @@
 
 namespace fmha_b200 {
 
-template <int kBN_>
-struct FwdCfgD256 {
-  static constexpr int D = 256;
+// Single-Q-tile, double-buffered-S configuration for head dim D and K/V
+// step kBN.  TMEM: S buffers [0,kBN) [kBN,2kBN), O [2kBN, 2kBN+D); the
+// allocation is the next power of two, so D + 2*kBN <= 256 fits two CTAs per
+// SM (their softmax warpgroups then share the SM like a ping-pong, without
+// the P -> PV -> S dependency chain between them).
+template <int D_, int kBN_>
+struct FwdCfgST {
+  static constexpr int D = D_;
   static constexpr int kBM = 128;
   static constexpr int kBN = kBN_;
   static_assert(kBN == 64 || kBN == 128, "K/V step of 64 or 128 rows");
-  static constexpr int kChunks = 4;
-  static constexpr int kQTileBytes = kBM * D * 2;    // 64 KB
-  static constexpr int kKVTileBytes = kBN * D * 2;   // 32 / 64 KB
-  static constexpr int kStages = kBN == 64 ? 4 : 2;
+  static_assert(D == 64 || D == 128 || D == 256, "head dim");
+  static constexpr int kChunks = D / 64;
+  static constexpr int kQTileBytes = kBM * D * 2;
+  static constexpr int kKVTileBytes = kBN * D * 2;
+  static constexpr uint32_t kColO = 2 * kBN;
+  static constexpr uint32_t kTmemCols = (2 * kBN + D) <= 256 ? 256u : 512u;
+  static constexpr int kCtasPerSm = kTmemCols == 256 ? 2 : 1;
+  static constexpr int kRingBudget = (kCtasPerSm == 2 ? 112 * 1024 : 226 * 1024) - kQTileBytes - 1024 - 256;
+  static constexpr int kStagesFit = kRingBudget / kKVTileBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static_assert(kStages >= 2, "K/V ring needs two slots");
   static constexpr int kSmemRing = kStages * kKVTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 2;
   static constexpr int kSmemBytes = kQTileBytes + kSmemRing + kNumBars * 8 + 16;
@@ -54,18 +67,17 @@ struct FwdCfgD256 {
   static constexpr int kLoadWarp = 4;
   static constexpr int kMmaWarp = 5;
   __host__ __device__ static constexpr uint32_t col_s(int buf) { return buf ? static_cast<uint32_t>(kBN) : 0u; }
-  static constexpr uint32_t kColO = 256;
-  static constexpr uint32_t kTmemCols = 512;
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
+template <int kBN_>
+using FwdCfgD256 = FwdCfgST<256, kBN_>;
 
-template <bool kBF16, int kBN = 128, int kEmuPer16 = 4>
-__global__ void __launch_bounds__(192, 1)
-    fmha_fwd_d256_kernel(const __grid_constant__ CUtensorMap tmQ,
-                         const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
-  using C = FwdCfgD256<kBN>;
-  constexpr int D = C::D;
+template <int D, bool kBF16, int kBN = 128, int kEmuPer16 = 4>
+__global__ void __launch_bounds__(192, FwdCfgST<D, kBN>::kCtasPerSm)
+    fmha_fwd_st_kernel(const __grid_constant__ CUtensorMap tmQ,
+                       const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+  using C = FwdCfgST<D, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -259,7 +271,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       const float neg = -m * sl2;
       const bool masked = valid < C::kBN;
-      uint32_t p[C::kBN / 2];
+      uint32_t p[32];
       float rs;
       if constexpr (C::kBN == 128) {
         uint32_t p0[32], p1[32];
