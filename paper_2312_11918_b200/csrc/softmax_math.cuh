@@ -97,9 +97,24 @@ __device__ __forceinline__ uint32_t pack2_x2(uint64_t e) {
   return pack2<kBF16>(lo, hi);
 }
 
+// Which score pairs take the polynomial: kEmuPer16 of every 16, spread evenly
+// (FMHA_EMU_SPREAD=1) so each polynomial chain on the FMA pipe runs beside
+// MUFU work, or clustered at the start of each group of 16 pairs (0).
+#ifndef FMHA_EMU_SPREAD
+#define FMHA_EMU_SPREAD 1
+#endif
+template <int kEmuPer16>
+__device__ __forceinline__ constexpr bool emulate_pair(int i) {
+#if FMHA_EMU_SPREAD
+  return kEmuPer16 > 0 && ((i & 15) * kEmuPer16) % 16 + kEmuPer16 >= 16;
+#else
+  return (i & 15) < kEmuPer16;
+#endif
+}
+
 // P = 2^(s*c - m*c) for the kCols scores s[kOff .. kOff+kCols) of one row;
 // returns the fp32 sum of the UNROUNDED P (attention.cpp:50-55) and writes
-// the 16-bit packed P.  Pairs with (i % 16) < kEmuPer16 use the polynomial.
+// the 16-bit packed P.  Pairs selected by emulate_pair use the polynomial.
 template <bool kBF16, int kOff, int kCols, int kEmuPer16, int kTotal>
 __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float c, float neg_mc,
                                                  uint32_t (&p)[kCols / 2]) {
@@ -109,7 +124,7 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
 #pragma unroll
   for (int i = 0; i < kCols / 2; ++i) {
     const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
-    const uint64_t e = ((i & 15) < kEmuPer16) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
     if (i & 1)
       acc1 = fadd2(acc1, e);
     else
