@@ -52,38 +52,12 @@
 
 #include <cuda.h>
 #include <cstdint>
-#include <type_traits>
 
 #include "sm100.cuh"
 #include "softmax_math.cuh"
 #include "tmem_ops.cuh"
 
-// Softmax publication variants (tuning knobs, fixed at build time)
-#ifndef FMHA_P_CHUNKS
-#define FMHA_P_CHUNKS 2  // P published in this many chunks of kv rows per tile
-#endif
-#ifndef FMHA_SPEC_MAX
-#define FMHA_SPEC_MAX 0  // exponentiate chunk 0 against the stale max while reducing the new one
-#endif
-#ifndef FMHA_MASKED_EXACT
-#define FMHA_MASKED_EXACT 1  // padded (masked) tiles take an all-MUFU copy of the exp code
-#endif
-#ifndef FMHA_MMA_SPIN
-#define FMHA_MMA_SPIN 0  // MMA warp spins (test_wait) on P instead of a suspending try_wait
-#endif
-#ifndef FMHA_DEFER_WAIT
-#define FMHA_DEFER_WAIT 1  // wait for chunk c's TMEM store only after chunk c+1's exps
-#endif
-
 namespace fmha_b200 {
-
-template <int I, int N, class F>
-__device__ __forceinline__ void static_for(F&& f) {
-  if constexpr (I < N) {
-    f(std::integral_constant<int, I>{});
-    static_for<I + 1, N>(f);
-  }
-}
 
 struct FwdArgs {
   void* o;                   // BSHD output (direct-store epilogue of the d=256 kernel)
@@ -126,7 +100,7 @@ struct FwdCfg {
   static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
   static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
-  static constexpr int kPChunks = FMHA_P_CHUNKS;    // P published in chunks of kv rows
+  static constexpr int kPChunks = 2;  // P published in two halves of 64 kv rows
   static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 6;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
@@ -312,10 +286,7 @@ __global__ void __launch_bounds__(384, 1)
         constexpr int kStepsPerChunk = 8 / C::kPChunks;
 #pragma unroll
         for (int c = 0; c < C::kPChunks; ++c) {
-          if constexpr (FMHA_MMA_SPIN)
-            mbar_wait_spin(&p_full[q * C::kPChunks + c], par);
-          else
-            mbar_wait(&p_full[q * C::kPChunks + c], par);
+          mbar_wait(&p_full[q * C::kPChunks + c], par);
           if (c == C::kPChunks - 1) trace_stamp(args, trp, q, jt, 11);
           tc_fence_after();
 #pragma unroll
@@ -457,89 +428,46 @@ __global__ void __launch_bounds__(384, 1)
           return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         };
-        // P chunk c = scores [c*kCW, (c+1)*kCW) -> kCW/2 packed columns of
-        // S_q's TMEM region (S is already in registers).
-        constexpr int kNC = C::kPChunks;
-        constexpr int kCW = 128 / kNC;
+        // Conditional rescale (exact, since the final (m, Sigma) pair is
+        // consistent): a warp keeps its stale max unless some row's max grew
+        // by more than 8 in log2 units (P stays <= 256).
+        {
+          const float mx = row_max();
+          trace_stamp(args, trq, q, j, 8);
+          if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
+            const float m_new = fmaxf(mx, m);
+            if (j == 0)
+              m = m_new;  // l = 0 and the first PV overwrites O
+            else
+              rescale(m_new);
+          }
+        }
+        // P half h = scores [64h, 64h+64) -> packed TMEM columns [32h, 32h+32)
+        // of S_q (S is already in registers).  Padded tiles take an all-MUFU
+        // copy (exact zeros for -inf scores).  The TMEM store of half 0 is
+        // waited for only after half 1's exponentials: the ~200-clk store
+        // latency leaves the critical path; GEMM-II on half 0 then overlaps
+        // the store and publication of half 1.
+        const float neg = -m * sl2;
         const bool masked = valid < C::kBN;
-        uint32_t pbuf[2][kCW / 2];
-        auto exp_chunk = [&](auto ci, float negv) -> float {
-          constexpr int c = decltype(ci)::value;
-#if FMHA_MASKED_EXACT
-          return masked ? exp_rowsum_pack<kBF16, c * kCW, kCW, 0>(s, sl2, negv, pbuf[c & 1])
-                        : exp_rowsum_pack<kBF16, c * kCW, kCW, kEmuPer16>(s, sl2, negv, pbuf[c & 1]);
-#else
-          (void)masked;
-          return exp_rowsum_pack<kBF16, c * kCW, kCW, kEmuPer16>(s, sl2, negv, pbuf[c & 1]);
-#endif
-        };
-        auto store_chunk = [&](auto ci) {
-          constexpr int c = decltype(ci)::value;
-          if constexpr (kCW / 2 == 16)
-            tmem_st32x32b_x16(tS + c * (kCW / 2), pbuf[c & 1]);
-          else
-            tmem_st32x32b_x32(tS + c * (kCW / 2), pbuf[c & 1]);
-        };
-        auto arrive_chunk = [&](int c) {
+        uint32_t p0[32], p1[32];
+        float rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
+                          : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+        trace_stamp(args, trq, q, j, 9);
+        tmem_st32x32b_x32(tS, p0);
+        rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
+                     : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        trace_stamp(args, trq, q, j, 10);
+        auto publish = [&](int half) {
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[q * kNC + c]);
+          if (lane == 0) mbar_arrive(&p_full[q * 2 + half]);
         };
-        float neg, rs;
-        if constexpr (FMHA_SPEC_MAX) {
-          // Speculative max: the first chunk is exponentiated against the
-          // running (stale) max while this tile's row max is reduced on the
-          // ALU pipe in parallel; recomputed only when the max moved.
-          neg = -m * sl2;
-          rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
-          const float mx = row_max();
-          trace_stamp(args, trq, q, j, 8);
-          if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
-            const float m_new = fmaxf(mx, m);
-            if (j == 0)
-              m = m_new;  // l = 0 and the first PV overwrites O
-            else
-              rescale(m_new);
-            neg = -m * sl2;
-            rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
-          }
-        } else {
-          // Conditional rescale (exact, since the final (m, Sigma) pair is
-          // consistent): a warp keeps its stale max unless some row's max
-          // grew by more than 8 in log2 units (P stays <= 256).
-          const float mx = row_max();
-          trace_stamp(args, trq, q, j, 8);
-          if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
-            const float m_new = fmaxf(mx, m);
-            if (j == 0)
-              m = m_new;  // l = 0 and the first PV overwrites O
-            else
-              rescale(m_new);
-          }
-          neg = -m * sl2;
-          rs = exp_chunk(std::integral_constant<int, 0>{}, neg);
-        }
-        trace_stamp(args, trq, q, j, 9);
-        static_for<0, kNC>([&](auto ci) {
-          constexpr int c = decltype(ci)::value;
-          store_chunk(ci);
-          if constexpr (c + 1 < kNC) {
-            if constexpr (FMHA_DEFER_WAIT) {
-              // the store of chunk c is waited for after the next chunk's
-              // exponentials: the TMEM write latency leaves the critical path
-              rs += exp_chunk(std::integral_constant<int, c + 1>{}, neg);
-              arrive_chunk(c);
-            } else {
-              arrive_chunk(c);
-              rs += exp_chunk(std::integral_constant<int, c + 1>{}, neg);
-            }
-          } else {
-            trace_stamp(args, trq, q, j, 10);
-            arrive_chunk(c);
-          }
-          if constexpr (c == 0) trace_stamp(args, trq, q, j, 2);
-        });
+        publish(0);
+        trace_stamp(args, trq, q, j, 2);
+        tmem_st32x32b_x32(tS + 32, p1);
+        publish(1);
         l += rs;
         trace_stamp(args, trq, q, j, 3);
 #ifdef FMHA_TRACE_BUILD
