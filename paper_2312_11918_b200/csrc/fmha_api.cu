@@ -126,7 +126,7 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
-  a.trace = trace_buffer(static_cast<size_t>(3 * a.n_kv_tiles * 16));
+  a.trace = trace_buffer(static_cast<size_t>(3 * a.n_kv_tiles * 16 + 64));
   const int grid = std::min(a.n_units, num_sms());
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();

@@ -304,6 +304,10 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t ue = (static_cast<uint32_t>(i) & 1) ^ 1;  // o_empty parity
         const int qs = i % C::kQStages;
         mbar_wait(&q_full[qs], static_cast<uint32_t>(i / C::kQStages) & 1);
+#ifdef FMHA_TRACE_BUILD
+        // per-unit timeline of CTA 0 (units 0..7): trace[(3*n_kv)*16 + i*8 + k]
+        if (tr && i < 8) args.trace[(3 * n_kv) * 16 + i * 8 + 0] = clock64();
+#endif
         sQ_addr = smem_u32(sQ) + qs * 2 * C::kQTileBytes;
         int ks = next_slot();
         tc_fence_after();
@@ -388,6 +392,9 @@ __global__ void __launch_bounds__(384, 1)
       for (int j = 0; j < n_kv; ++j, ++it) {
         mbar_wait(&s_full[q], it & 1);
         trace_stamp(args, trq, q, j, 0);
+#ifdef FMHA_TRACE_BUILD
+        if (tr && i < 8 && r == 0 && j == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 1 + q] = clock64();
+#endif
         tc_fence_after();
         uint32_t sr[128];
         tmem_ld32x32b_x128(tS, sr);
@@ -516,6 +523,9 @@ __global__ void __launch_bounds__(384, 1)
       if (row < N && args.lse != nullptr)
         args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
       trace_stamp(args, trq, q, n_kv - 1, 7);
+#ifdef FMHA_TRACE_BUILD
+      if (tr && i < 8 && r == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 3 + q] = clock64();
+#endif
     }
   }
 

@@ -1,7 +1,8 @@
-"""Debug: per-K/V-tile timeline of CTA 0's first work unit (FMHA_TRACE=1).
+"""Debug: per-K/V-tile timeline of CTA 0's first work unit (FMHA_TRACE=1),
+per-warp completion skew, and the per-unit timeline of CTA 0.
 
 Run on a GPU (needs `make trace`):
-    FMHA_TRACE=1 python tools/trace_timeline.py [N] [d]
+    FMHA_TRACE=1 python tools/trace_timeline.py [N] [d] [L] [h]
 
 Slots per (Q tile q, K/V tile j), see FwdArgs::trace in fmha_fwd_kernel.cuh:
  softmax WG q: 0 woke (S ready)  1 S in registers  8 row max done  9 first-half exps
@@ -23,16 +24,18 @@ import paper_2312_11918_b200 as fm  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-L, h = 4, 16
+L = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+h = int(sys.argv[4]) if len(sys.argv) > 4 else 16
 q, k, v = (torch.randn(L, N, h, d, device="cuda").half() for _ in range(3))
 for _ in range(3):
     fm.fmha_fwd(q, k, v)
 torch.cuda.synchronize()
 S = 16
 n_kv = (N + 127) // 128
-buf = np.zeros(3 * n_kv * S, np.uint64)
+buf = np.zeros(3 * n_kv * S + 64, np.uint64)
 fm.lib().fmha_debug_trace_copy(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size)
-full = buf.reshape(-1, n_kv, S).astype(np.int64)
+full = buf[:3 * n_kv * S].reshape(-1, n_kv, S).astype(np.int64)
+units = buf[3 * n_kv * S: 3 * n_kv * S + 64].reshape(8, 8).astype(np.int64)
 t = full[:2]
 warp_t = full[2].astype(np.int64)
 start, setup = t[0, 0, 6], t[0, 0, 7]
@@ -44,14 +47,15 @@ SEG = [  # (name, from slot, to slot, same j?)
     ("S issue", 12, 5),
 ]
 print(f"N={N} d={d} n_kv={n_kv}  setup {setup - start} clk, first S ready q0 {t[0,0,0]} q1 {t[1,0,0]}")
-lo, hi = 2, n_kv - 2
+lo, hi = min(2, n_kv - 1), max(n_kv - 2, min(2, n_kv - 1) + 1)
 for name, a, b in SEG:
     vals = t[:, lo:hi, b] - t[:, lo:hi, a]
     print(f"  {name:22s} median q0 {np.median(vals[0]):6.0f}  q1 {np.median(vals[1]):6.0f}")
 issue_to_next = t[:, lo + 1:hi + 1, 0] - t[:, lo:hi, 5]
 print(f"  {'S issued->next wake':22s} median q0 {np.median(issue_to_next[0]):6.0f}  q1 {np.median(issue_to_next[1]):6.0f}")
 per = np.diff(t[0, lo:hi, 0])
-print(f"steady-state period per K/V tile: median {np.median(per):.0f} clk, min {per.min()}")
+if per.size:
+    print(f"steady-state period per K/V tile: median {np.median(per):.0f} clk, min {per.min()}")
 # overlap of the two softmax WGs' busy intervals [in regs, published]
 busy0 = [(t[0, j, 1], t[0, j, 3]) for j in range(lo, hi)]
 busy1 = [(t[1, j, 1], t[1, j, 3]) for j in range(lo, hi)]
@@ -85,3 +89,10 @@ for j in range(4, min(10, n_kv)):
         ws = [4 * qq + x for x in range(4)]
         base = min(w[j, x] for x in ws)
         print(f"  j{j} q{qq}: " + " ".join(f"w{x}:{w[j, x] - base:5d}" for x in ws))
+
+print("\nper-unit timeline of CTA 0 (clk since kernel start): Q ready at MMA | first S ready q0 q1 | epilogue done q0 q1")
+for i in range(8):
+    if units[i, 0] == 0:
+        break
+    x = [v - start if v > 0 else -1 for v in units[i, :5]]
+    print(f"  unit {i}: {x[0]:8d} | {x[1]:8d} {x[2]:8d} | {x[3]:8d} {x[4]:8d}")
