@@ -1,0 +1,68 @@
+"""§8 row f4: the reference's memsim traffic model vs the kernel's measured DRAM bytes.
+
+The reference's `run_fmha_traced` (proj/src/memsim.cpp:160-197) charges, per (b, head):
+  Q  = N*d*e            (each Q tile read once)
+  K  = V = ceil(N/bM) * N*d*e   (every Q tile re-reads all of K and V: no reuse beyond shared memory)
+  O  = N*d*e_o          (written once)
+pinned by proj/tests/test_memsim.cpp:75-86.  This kernel shares each K/V tile between the two Q
+tiles of a work unit (effective bM = 256 at d <= 128, 128 at d = 256) and orders the persistent
+grid so co-resident CTAs work on the same heads (K/V re-reads hit L2).  The table compares the
+memsim reads at the reference's bM and at the kernel's effective bM with the compulsory bytes
+(Q + K + V once) and the ncu-measured DRAM reads (profiles/r01e_*_ncu_full.txt).
+
+    python tools/traffic_model.py
+"""
+import json
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIGS = {"c1": (1, 512, 1, 64), "c2": (16, 512, 12, 64), "c3": (4, 4096, 16, 128),
+           "c4": (2, 8192, 8, 256), "c5": (8, 16384, 32, 128)}
+
+
+def memsim_bytes(L, N, h, d, bM, e=2, e_o=2):
+    """Gmem bytes of the reference's traced fused run (memsim.cpp:174-186)."""
+    q_tiles = -(-N // bM)
+    per_head_q = N * d * e
+    per_head_kv = q_tiles * N * d * e
+    reads = L * h * (per_head_q + 2 * per_head_kv)
+    writes = L * h * N * d * e_o
+    return reads, writes
+
+
+UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def measured_reads(cfg):
+    """ncu dram__bytes_read.sum of the committed profile for this config, in bytes."""
+    for name in (f"r01e_{cfg}_ncu_full.txt", f"r01e_{cfg}_ncu_dram.txt"):
+        p = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(p):
+            continue
+        for line in open(p):
+            m = re.search(r"dram__bytes_read\.sum\s+(?:(\w*byte)\s+([\d.,]+)|([\d.,]+)\s+(\w*byte))", line)
+            if m:
+                unit = m.group(1) or m.group(4)
+                val = m.group(2) or m.group(3)
+                return float(val.replace(",", "")) * UNITS[unit]
+    return None
+
+
+def main():
+    print(f"{'cfg':4s} {'memsim bM=128':>15s} {'memsim bM=eff':>15s} {'compulsory':>12s} {'ncu DRAM rd':>12s}  (MB)")
+    rows = {}
+    for c, (L, N, h, d) in CONFIGS.items():
+        r128, _ = memsim_bytes(L, N, h, d, 128)
+        eff = 256 if d <= 128 else 128
+        reff, _ = memsim_bytes(L, N, h, d, eff)
+        comp = 3 * L * N * h * d * 2
+        meas = measured_reads(c)
+        rows[c] = dict(memsim_bM128=r128, memsim_eff=reff, compulsory=comp, measured=meas)
+        ms = f"{meas / 1e6:12.1f}" if meas else f"{'-':>12s}"
+        print(f"{c:4s} {r128 / 1e6:15.1f} {reff / 1e6:15.1f} {comp / 1e6:12.1f} {ms}")
+    return rows
+
+
+if __name__ == "__main__":
+    main()
