@@ -324,12 +324,15 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
   const bool bf = p->dtype == FMHA_BF16;
   switch (p->d) {
     case 64: {
-      // FMHA_TUNE_EMU64 selects the exp2 split for tuning runs (pairs of 16
-      // on the polynomial; default 4)
-      static const int emu64 = [] {
+      // exp2 split (pairs of 16 on the polynomial): at d=64 the tensor core
+      // has slack, so long sequences move more exponentials to the FMA pipe
+      // (6/16: L=4,h=32,N=4096 686 -> 730 TFLOP/s); short ones keep 4/16.
+      // FMHA_TUNE_EMU64 overrides for tuning runs.
+      static const int emu64_env = [] {
         const char* e = std::getenv("FMHA_TUNE_EMU64");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : -1;
       }();
+      const int emu64 = emu64_env >= 0 ? emu64_env : (p->N >= 1024 ? 6 : 4);
       if (emu64 == 0)
         return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st)
                   : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st);

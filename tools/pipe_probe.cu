@@ -100,6 +100,31 @@ __device__ __forceinline__ float exp_sum_h16(const float (&s)[128], float c, flo
   return f.x + f.y + fs;
 }
 
+// half-0 exponentials with the full-row max folded into the same loop (the
+// kernel's "speculative max" formulation): 4 scores per iteration into 8 chains
+template <int EMU, int kOff>
+__device__ __forceinline__ float exp_half_with_max(const float (&s)[128], float c, float nm, uint32_t (&p)[32],
+                                                   float& row_max) {
+  const uint64_t c2 = f2_pack(c, c), nm2 = f2_pack(nm, nm);
+  uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = f2_pack(0.f, 0.f);
+  float mx[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) mx[t] = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
+    mx[i & 7] = fmaxf(mx[i & 7], fmaxf(fmaxf(s[4 * i], s[4 * i + 1]), fmaxf(s[4 * i + 2], s[4 * i + 3])));
+    const uint64_t e = emulate_pair<EMU>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    if (i & 1) acc1 = fadd2(acc1, e); else acc0 = fadd2(acc0, e);
+    p[i] = pack2_x2<false>(e);
+  }
+  row_max = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+  float a0, a1, b0, b1;
+  f2_unpack(acc0, a0, a1);
+  f2_unpack(acc1, b0, b1);
+  return (a0 + b0) + (a1 + b1);
+}
+
 __device__ __forceinline__ float row_max128(const float (&s)[128]) {
   float mx[8];
 #pragma unroll
@@ -133,10 +158,21 @@ __global__ void __launch_bounds__(256, 1) probe(const float* in, uint32_t* out, 
       const float4 v = *reinterpret_cast<const float4*>(src + i);
       s[i] = v.x; s[i + 1] = v.y; s[i + 2] = v.z; s[i + 3] = v.w;
     }
-    const float m = row_max128(s);
-    const float nm = -m * c;
     uint32_t p[32];
     uint32_t* dst = sh_p + threadIdx.x * 36;
+    if (MODE == 6) {  // speculative: exps of half 0 against a stale max, row max interleaved
+      float mrow;
+      const float nm0 = -0.5f * c;
+      sum += exp_half_with_max<EMU, 0>(s, c, nm0, p, mrow);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) st_shared_v4(dst + i, p[i], p[i + 1], p[i + 2], p[i + 3]);
+      sum += exp_rowsum_pack<false, 64, 64, EMU>(s, c, -mrow * c, p);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) st_shared_v4(dst + i, p[i], p[i + 1], p[i + 2], p[i + 3]);
+      continue;
+    }
+    const float m = row_max128(s);
+    const float nm = -m * c;
     if (MODE == 0) {
       sum += exp_rowsum_pack<false, 0, 64, EMU>(s, c, nm, p);
     } else if (MODE == 5) {
@@ -186,12 +222,10 @@ void run(int threads, const char* name) {
 
 int main() {
   for (int t : {128, 256}) {
-    run<0, 0>(t, "packed f32 deg3 (16ths)");
-    run<0, 1>(t, "packed f32 deg3 (16ths)");
-    run<0, 2>(t, "packed f32 deg3 (16ths)");
-    run<0, 3>(t, "packed f32 deg3 (16ths)");
-    run<0, 4>(t, "packed f32 deg3 (16ths)");
-    run<0, 6>(t, "packed f32 deg3 (16ths)");
+    run<0, 4>(t, "max then exps (kernel)");
+    run<6, 4>(t, "speculative, max interleaved");
+    run<0, 6>(t, "max then exps (kernel)");
+    run<6, 6>(t, "speculative, max interleaved");
   }
   return 0;
 }
