@@ -135,15 +135,6 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   return FMHA_OK;
 }
 
-// K/V step of the d=256 kernel (FMHA_D256_BN=64 selects the 64-row variant, for A/B runs)
-int d256_bn() {
-  static const int bn = [] {
-    const char* e = std::getenv("FMHA_D256_BN");
-    return (e && std::atoi(e) == 64) ? 64 : 128;
-  }();
-  return bn;
-}
-
 template <int D, bool BF16, int BN>
 fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
                       const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
@@ -313,7 +304,7 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
     return fail(FMHA_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
   const int rows = 128;
-  const int kv_rows = p->d == 256 ? d256_bn() : 128;
+  const int kv_rows = 128;  // K/V TMA box rows (d = 256 also streams 128-row K/V steps)
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, p->dtype, p, p->q_stride, rows) ||
       !make_map(&mk, k, p->dtype, p, p->k_stride, kv_rows) ||
@@ -367,8 +358,6 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
     default:
-      if (d256_bn() == 64)
-        return bf ? launch_st<256, true, 64>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 64>(p, mq, mk, mv, o, lse, st);
       return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st);
   }
 }
