@@ -287,6 +287,9 @@ fmha_status fmha_fwd_check(const fmha_fwd_params* p) {
                                           " unsupported by the sm_100a kernel (64, 128, 256)");
   if (p->N > (1ll << 31) - 256 || p->h > 65535 || p->L > 65535)
     return fail(FMHA_ERR_UNSUPPORTED, "problem too large for the launch grid");
+  // the persistent kernels index work units (256 query rows of one head) with int32
+  if (((p->N + 255) / 256) * p->h * p->L > (1ll << 31) - 1)
+    return fail(FMHA_ERR_UNSUPPORTED, "problem too large: more than 2^31 work units");
   const int64_t* strides[4] = {p->q_stride, p->k_stride, p->v_stride, p->o_stride};
   for (auto s : strides)
     for (int i = 0; i < 3; ++i)

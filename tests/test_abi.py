@@ -70,6 +70,10 @@ def test_check_validation():
     p = fm.dense_params(1, 64, 1, 64)
     p.dtype = 7
     assert _check(p) == fm.ERR_CONFIG
+    # grid limits: h, L <= 65535 and < 2^31 work units of 256 query rows
+    assert _check(fm.dense_params(1, 256, 65536, 64)) == fm.ERR_UNSUPPORTED
+    assert _check(fm.dense_params(65535, 1 << 24, 65535, 64)) == fm.ERR_UNSUPPORTED
+    assert b"work units" in fm.lib().fmha_last_error()
 
 
 def test_fwd_rejects_null_before_launch():
