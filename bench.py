@@ -361,7 +361,7 @@ def measure_e2e(fm, q, k, v, cfg, args, world, dev):
     bo = ho.numel() * ho.element_size() + hl.numel() * 4
     # the e2e roofline: host->device copy of the inputs at this box's measured
     # pinned H2D rate (the D2H of O/LSE overlaps it; PCIe is full duplex)
-    pcie = measure_h2d_gbps(dev)
+    pcie = measure_h2d_gbps(dev, hq)
     bound_ms = bi / (pcie * 1e9) * 1e3
     return {"value": world * flops(L, N, h, d) * steps / dt / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": steps,
@@ -371,18 +371,23 @@ def measure_e2e(fm, q, k, v, cfg, args, world, dev):
             "api": "fmha_fwd_host (C ABI, pinned host 16-bit buffers; 3-stream H2D/kernel/D2H pipeline)"}
 
 
-def measure_h2d_gbps(dev, mb=128, reps=3):
-    """Pinned host->device copy rate on this box (GB/s), contiguous."""
+def measure_h2d_gbps(dev, host, reps=5):
+    """Pinned host->device copy rate on this box (GB/s): contiguous copies of
+    `host` (a pinned buffer the e2e loop already used), timed with CUDA events
+    after warm-up."""
     import torch
-    hbuf = torch.empty(mb << 20, dtype=torch.uint8).pin_memory()
-    dbuf = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
-    dbuf.copy_(hbuf, non_blocking=True)
+    dbuf = torch.empty(host.numel() * host.element_size(), dtype=torch.uint8, device=dev)
+    src = host.view(-1).view(torch.uint8)
+    for _ in range(3):
+        dbuf.copy_(src, non_blocking=True)
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
     for _ in range(reps):
-        dbuf.copy_(hbuf, non_blocking=True)
+        dbuf.copy_(src, non_blocking=True)
+    e.record()
     torch.cuda.synchronize(dev)
-    return reps * (mb << 20) / (time.perf_counter() - t0) / 1e9
+    return reps * src.numel() / (s.elapsed_time(e) * 1e-3) / 1e9
 
 
 def main():
