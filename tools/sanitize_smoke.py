@@ -1,0 +1,13 @@
+"""Small ragged/bf16/d=256 cases for compute-sanitizer runs:
+    compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_smoke.py
+Results and their reading: DESIGN.md §10."""
+import os, sys, torch
+sys.path.insert(0, os.getcwd())
+import paper_2312_11918_b200 as fm
+torch.manual_seed(0)
+for (L, N, h, d, dt) in [(1, 200, 2, 64, torch.float16), (2, 333, 3, 128, torch.bfloat16), (1, 1000, 2, 256, torch.float16), (3, 130, 1, 128, torch.float16), (1, 1, 1, 64, torch.float16)]:
+    q, k, v = (torch.randn(L, N, h, d, device="cuda", dtype=dt) for _ in range(3))
+    o, lse = fm.fmha_fwd(q, k, v)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2).float(), k.transpose(1, 2).float(), v.transpose(1, 2).float()).transpose(1, 2)
+    print(L, N, h, d, dt, "max err", (o.float() - ref).abs().max().item(), flush=True)
