@@ -101,7 +101,7 @@ struct FwdCfg {
   static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
   static constexpr int kPChunks = 2;  // P published in two halves of 64 kv rows
-  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 6;
+  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 7;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
   static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = s_full + 2;             // [2][kPChunks]: (tile q, chunk of kv rows)
   uint64_t* o_full = p_full + 2 * C::kPChunks;  // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
-  uint64_t* stage_free = o_empty + 2;        // O staging tile read by its TMA store
-  uint64_t* stage_ready = stage_free + 1;    // O staging tile written by a softmax WG
+  uint64_t* stage_free = o_empty + 2;        // [2]: WG q's use of the O staging tile read by its TMA store
+  uint64_t* stage_ready = stage_free + 2;    // O staging tile written by a softmax WG
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&o_full[q], 1);
       mbar_init(&o_empty[q], 4);
     }
-    mbar_init(stage_free, 1);
+    mbar_init(&stage_free[0], 1);
+    mbar_init(&stage_free[1], 1);
     mbar_init(stage_ready, 4);
     fence_mbar_init();
   }
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(384, 1)
               tma_store_4d(&tmO, sO + c * C::kBM * 128, c * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
             tma_store_commit();
             tma_store_wait_read();
-            mbar_arrive(stage_free);
+            mbar_arrive(&stage_free[q]);
           }
         }
         tma_store_wait_all();
@@ -490,11 +491,15 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&o_full[q], i & 1);
       tc_fence_after();
       trace_stamp(args, trq, q, n_kv - 1, 6);
-      // The two WGs take the staging tile in turn (WG0 unit i, WG1 unit i,
-      // WG0 unit i+1, ...): wait until the previous user's TMA store has
-      // read it.  Completion #k of stage_free is the k-th use, so WG0 waits
-      // for odd completions and WG1 for even ones.
-      mbar_wait(stage_free, q ? 0u : 1u);
+      // The two WGs take the staging tile in strict turns (WG0 unit i, WG1
+      // unit i, WG0 unit i+1, ...): before writing, wait until the OTHER
+      // WG's latest use has been read by its TMA store.  That use itself
+      // waited for this WG's previous use, so stage_free[q^1] is at most one
+      // phase away from the awaited one and the parity wait is exact.
+      if (q == 1)
+        mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
+      else if (i > 0)
+        mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
       const float inv = 1.0f / l;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
