@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=120.0,
+                    help="reference arm: CPU-time budget for the whole --warmup + --steps run")
     return ap.parse_args()
 
 
@@ -194,7 +196,7 @@ def run_reference(args):
     cfg, local, scaling, global_L = workload(args.config, 1, 0)
     threads = orc.default_threads()
     # per-step sample sized so W + K steps stay within ~2 minutes
-    per_step_budget = 120.0 / max(1, args.steps + args.warmup)
+    per_step_budget = args.ref_seconds / max(1, args.steps + args.warmup)
     probe = cpu_baseline(cfg, threads, mode="1")
     tiles_per_thread = max(1, int(per_step_budget / max(probe["seconds"], 1e-3)))
     for _ in range(args.warmup):
