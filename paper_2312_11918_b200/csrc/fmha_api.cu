@@ -18,6 +18,7 @@
 
 #include "../../include/fmha/fmha.h"
 #include "fmha_errors.hpp"
+#include "fmha_fwd_pair_kernel.cuh"
 #include "fmha_fwd_st_kernel.cuh"
 #include "fmha_fwd_kernel.cuh"
 
@@ -131,6 +132,52 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  g_last_launches = 1;
+  return FMHA_OK;
+}
+
+// d = 256 on CTA pairs (cluster 2 x 1 x 1 over the Q-tile axis; needs an even
+// number of 128-row Q tiles).  `mk64` is a K map with 64-row boxes.
+template <bool BF16>
+fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
+                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+  using Cfg = fmha_b200::FwdCfgPair;
+  auto kern = fmha_b200::fmha_fwd_pair_kernel<BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemAlloc);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set = true;
+  }
+  fmha_b200::FwdArgs a{};
+  a.o = o;
+  a.lse = lse;
+  a.o_sb = p->o_stride[0];
+  a.o_sn = p->o_stride[1];
+  a.o_sh = p->o_stride[2];
+  a.N = static_cast<int>(p->N);
+  a.H = static_cast<int>(p->h);
+  a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
+  a.scale = resolve_scale(p);
+  a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
+                     static_cast<unsigned>(p->L));
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemAlloc;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mk64, mv, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch (CTA pair)");
   g_last_launches = 1;
   return FMHA_OK;
 }
@@ -360,8 +407,22 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
-    default:
+    default: {
+      // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound);
+      // they pair adjacent Q tiles, so the tile count must be even.
+      // FMHA_TUNE_PAIR=0 forces the single-CTA kernel (A/B runs).
+      static const bool pair_ok = [] {
+        const char* e = std::getenv("FMHA_TUNE_PAIR");
+        return !(e && std::atoi(e) == 0);
+      }();
+      if (pair_ok && ((p->N + 127) / 128) % 2 == 0) {
+        CUtensorMap mk64;
+        if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
+          return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
+        return bf ? launch_pair<true>(p, mq, mk64, mv, o, lse, st) : launch_pair<false>(p, mq, mk64, mv, o, lse, st);
+      }
       return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st);
+    }
   }
 }
 

@@ -93,12 +93,15 @@ def test_custom_scale(oracle):
     _full_check(oracle, 1, 256, 2, 128, "f16", scale=0.05)
 
 
-def test_strided_views(oracle):
+@pytest.mark.parametrize("d,N", [(128, 384), (256, 512)], ids=["d128", "d256-pair"])
+def test_strided_views(oracle, d, N):
     """Q/K/V as views into one packed (L, N, 3, h, d) buffer and O into a
-    padded buffer: the ABI's explicit strides (head-sharding path, 8(e))."""
+    padded buffer: the ABI's explicit strides (head-sharding path, 8(e)).
+    d = 256 with an even Q-tile count runs the CTA-pair kernel (its K map has
+    64-row boxes over the same strides)."""
     import torch
     import paper_2312_11918_b200 as fm
-    L, N, h, d = 2, 384, 3, 128
+    L, h = 2, 3
     q, k, v = oracle.problem(L, N, h, d, 11, dtype="bf16")
     packed = torch.from_numpy(np.stack([q, k, v], axis=2)).cuda().to(torch.bfloat16)
     out = torch.zeros((L, N, h + 1, d), dtype=torch.bfloat16, device="cuda")
