@@ -136,8 +136,9 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   return FMHA_OK;
 }
 
-// d = 256 on CTA pairs (cluster 2 x 1 x 1 over the Q-tile axis; needs an even
-// number of 128-row Q tiles).  `mk64` is a K map with 64-row boxes.
+// d = 256 on CTA pairs (cluster 2 x 1 x 1 over the Q-tile axis).  An odd
+// Q-tile count gets one padding CTA per (b, head): its Q rows are all past N
+// (TMA zero-fills them, nothing is stored).  `mk64` is a K map with 64-row boxes.
 template <bool BF16>
 fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
                         const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
@@ -163,8 +164,8 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.scale_log2 = a.scale * 1.4426950408889634f;
   a.trace = nullptr;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
-                     static_cast<unsigned>(p->L));
+  const unsigned n_qtiles = static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM);
+  cfg.gridDim = dim3((n_qtiles + 1) & ~1u, static_cast<unsigned>(p->h), static_cast<unsigned>(p->L));
   cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmemAlloc;
   cfg.stream = st;
@@ -408,14 +409,15 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
     }
     default: {
-      // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound);
-      // they pair adjacent Q tiles, so the tile count must be even.
+      // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound).
+      // They pair adjacent Q tiles; a single Q tile (N <= 128) would pay a
+      // whole padding CTA, so it stays on the single-CTA kernel.
       // FMHA_TUNE_PAIR=0 forces the single-CTA kernel (A/B runs).
       static const bool pair_ok = [] {
         const char* e = std::getenv("FMHA_TUNE_PAIR");
         return !(e && std::atoi(e) == 0);
       }();
-      if (pair_ok && ((p->N + 127) / 128) % 2 == 0) {
+      if (pair_ok && p->N > 128) {
         CUtensorMap mk64;
         if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
           return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
