@@ -136,14 +136,14 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   return FMHA_OK;
 }
 
-// d = 256 on CTA pairs (cluster 2 x 1 x 1 over the Q-tile axis).  An odd
+// CTA-pair kernels (cluster 2 x 1 x 1 over the Q-tile axis).  An odd
 // Q-tile count gets one padding CTA per (b, head): its Q rows are all past N
 // (TMA zero-fills them, nothing is stored).  `mk64` is a K map with 64-row boxes.
-template <bool BF16>
+template <int D, int BN, bool BF16, int EMU>
 fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
                         const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
-  using Cfg = fmha_b200::FwdCfgPair;
-  auto kern = fmha_b200::fmha_fwd_pair_kernel<BF16>;
+  using Cfg = fmha_b200::FwdCfgPair<D, BN>;
+  auto kern = fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -364,6 +364,23 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or arguments)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool bf = p->dtype == FMHA_BF16;
+  // FMHA_TUNE_PAIR=0 keeps every head dim off the CTA-pair kernels (A/B runs)
+  static const bool pair_ok = [] {
+    const char* e = std::getenv("FMHA_TUNE_PAIR");
+    return !(e && std::atoi(e) == 0);
+  }();
+  // d = 128, long sequences: one Q tile per CTA with double-buffered 64-column
+  // S (no S -> softmax -> PV chain), two CTAs per SM, CTA pairs sharing K/V.
+  // Measured against the persistent ping-pong kernel: +2 % at N = 8192, +3.5 %
+  // at 16384 (+6 % on c5); -1 % at 4096 and -5..-10 % below (per-CTA prologue
+  // and epilogue of the non-persistent grid), so shorter sequences stay there.
+  if (p->d == 128 && pair_ok && p->N >= 8192) {
+    CUtensorMap mkh, mvh;
+    if (!make_map(&mkh, k, p->dtype, p, p->k_stride, 32) || !make_map(&mvh, v, p->dtype, p, p->v_stride, 64))
+      return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
+    return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st)
+              : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st);
+  }
   switch (p->d) {
     case 64: {
       // exp2 split (pairs of 16 on the polynomial): at d=64 the tensor core
@@ -412,16 +429,12 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound).
       // They pair adjacent Q tiles; a single Q tile (N <= 128) would pay a
       // whole padding CTA, so it stays on the single-CTA kernel.
-      // FMHA_TUNE_PAIR=0 forces the single-CTA kernel (A/B runs).
-      static const bool pair_ok = [] {
-        const char* e = std::getenv("FMHA_TUNE_PAIR");
-        return !(e && std::atoi(e) == 0);
-      }();
       if (pair_ok && p->N > 128) {
         CUtensorMap mk64;
         if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
           return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
-        return bf ? launch_pair<true>(p, mq, mk64, mv, o, lse, st) : launch_pair<false>(p, mq, mk64, mv, o, lse, st);
+        return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st)
+                  : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st);
       }
       return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st);
     }

@@ -1,4 +1,6 @@
-// fmha_fwd_pair_kernel.cuh -- head dim 256 on a CTA pair (cta_group::2).
+// fmha_fwd_pair_kernel.cuh -- forward pass on CTA pairs (cta_group::2): head
+// dim 256 (kBN = 128, one CTA per SM) and head dim 128 at long sequence
+// lengths (kBN = 64, two CTAs of different pairs per SM).
 //
 // Same contract as the other forward kernels (fmhasim::fmha_forward,
 // /root/reference/proj/src/attention.cpp:153-173); same per-CTA structure as
@@ -38,21 +40,31 @@
 
 namespace fmha_b200 {
 
+// Head dim D, K/V step kBN.  TMEM per CTA: S buffers [0,kBN) [kBN,2kBN),
+// O [2kBN, 2kBN+D), allocated as the next power of two; 2kBN + D <= 256
+// fits two CTAs (of two different pairs) per SM.
+template <int D_, int kBN_>
 struct FwdCfgPair {
-  static constexpr int D = 256;
+  static constexpr int D = D_;
   static constexpr int kBM = 128;  // Q rows per CTA (256 per pair)
-  static constexpr int kBN = 128;  // K/V rows per step
+  static constexpr int kBN = kBN_;  // K/V rows per step
+  static_assert(D == 128 || D == 256, "V is split into 64-column chunks per CTA");
+  static_assert(kBN == 64 || kBN == 128, "K/V step");
   static constexpr int kChunks = D / 64;
-  static constexpr int kQTileBytes = kBM * D * 2;          // 64 KB
-  static constexpr int kSlotBytes = kBN * D * 2 / 2;       // 32 KB: half a K or V tile
+  static constexpr int kQTileBytes = kBM * D * 2;
+  static constexpr int kSlotBytes = kBN * D * 2 / 2;       // half a K or V tile
   static constexpr int kKRowsPerCta = kBN / 2;             // K split by kv rows
   static constexpr int kVColsPerCta = D / 2;               // V split by head-dim columns
-  static constexpr int kStages = 5;
+  static constexpr uint32_t kTmemCols = (2 * kBN + D) <= 256 ? 256u : 512u;
+  static constexpr int kCtasPerSm = kTmemCols == 256 ? 2 : 1;
+  static constexpr int kRingBudget = (kCtasPerSm == 2 ? 112 * 1024 : 226 * 1024) - kQTileBytes - 1024 - 256;
+  static constexpr int kStagesFit = kRingBudget / kSlotBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static_assert(kStages >= 2, "K/V ring needs two slots");
   static constexpr int kSmemRing = kStages * kSlotBytes;
   static constexpr int kNumBars = 1 + 2 * kStages + 2 + 2 + 2;
   static constexpr int kSmemBytes = kQTileBytes + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;
-  static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kColO = 2 * kBN;
   static constexpr int kThreads = 192;
   static constexpr int kLoadWarp = 4;
@@ -61,13 +73,13 @@ struct FwdCfgPair {
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16, int kEmuPer16 = 4>
-__global__ void __launch_bounds__(192, 1)
+template <int D_, int kBN_, bool kBF16, int kEmuPer16 = 4>
+__global__ void __launch_bounds__(192, FwdCfgPair<D_, kBN_>::kCtasPerSm)
     fmha_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ,  // box 128 rows
-                         const __grid_constant__ CUtensorMap tmK,  // box 64 rows
-                         const __grid_constant__ CUtensorMap tmV,  // box 128 rows
+                         const __grid_constant__ CUtensorMap tmK,  // box kBN/2 rows
+                         const __grid_constant__ CUtensorMap tmV,  // box kBN rows
                          const FwdArgs args) {
-  using C = FwdCfgPair;
+  using C = FwdCfgPair<D_, kBN_>;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -250,7 +262,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&s_full[buf], static_cast<uint32_t>(j >> 1) & 1);
       tc_fence_after();
       uint32_t sr[C::kBN];
-      tmem_ld32x32b_x128(tS, sr);
+      if constexpr (C::kBN == 128)
+        tmem_ld32x32b_x128(tS, sr);
+      else
+        tmem_ld32x32b_x64(tS, sr);
       float s[C::kBN];
 #pragma unroll
       for (int c = 0; c < C::kBN; ++c) s[c] = __uint_as_float(sr[c]);
@@ -289,13 +304,16 @@ __global__ void __launch_bounds__(192, 1)
       }
       const float neg = -m * sl2;
       const bool masked = valid < C::kBN;
-      uint32_t p0[32], p1[32];
+      uint32_t p0[32];
       float rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
                         : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
       tmem_st32x32b_x32(tS, p0);
-      rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
-                   : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
-      tmem_st32x32b_x32(tS + 32, p1);
+      if constexpr (C::kBN == 128) {
+        uint32_t p1[32];
+        rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
+                     : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        tmem_st32x32b_x32(tS + 32, p1);
+      }
       l += rs;
       tmem_wait_st();
       tc_fence_before();

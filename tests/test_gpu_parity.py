@@ -115,7 +115,9 @@ def test_strided_views(oracle, d, N):
 
 
 @pytest.mark.parametrize("cfg", [(4, 4096, 16, 128, "f16"), (2, 8192, 8, 256, "f16"),
-                                 (8, 16384, 32, 128, "bf16")], ids=["c3", "c4", "c5"])
+                                 (8, 16384, 32, 128, "bf16"), (1, 8320, 2, 128, "f16"),
+                                 (1, 2432, 3, 256, "bf16")],
+                         ids=["c3", "c4", "c5", "d128-pair-odd-tiles", "d256-pair-odd-tiles"])
 def test_large_configs_sampled(oracle, cfg):
     """c3/c4/c5 at full size: inputs generated on the device (seeded torch
     RNG, rounded to the 16-bit type), every (b, head) computed on the GPU,
