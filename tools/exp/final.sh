@@ -7,3 +7,4 @@ ncu --set full --clock-control none --import-source on -k regex:fmha_fwd -s 3 -c
 ncu --set full --clock-control none -k regex:fmha_fwd -s 3 -c 1 -o gpurun_out/prof_c4 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 1 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_torchrun.json 2>/dev/null; cut -c1-200 gpurun_out/bench_torchrun.json
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>/dev/null; cut -c1-200 gpurun_out/bench_ref.json
+ncu --set full --clock-control none -k regex:fmha_fwd -s 3 -c 1 -o gpurun_out/prof_c5 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1

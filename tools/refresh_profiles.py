@@ -41,7 +41,7 @@ def main(tag):
     shutil.copy(os.path.join(OUT, "sweep.txt"), os.path.join(PROF, f"{tag}_table1_sweep.txt"))
     summary_path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
-    for c in ("c3", "c4"):
+    for c in ("c3", "c4", "c5"):
         rep = os.path.join(OUT, f"prof_{c}.ncu-rep")
         if not os.path.exists(rep):
             continue

@@ -36,8 +36,10 @@ UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 def measured_reads(cfg):
     """ncu dram__bytes_read.sum of the committed profile for this config, in bytes."""
-    for name in (f"r01e_{cfg}_ncu_full.txt", f"r01e_{cfg}_ncu_dram.txt"):
-        p = os.path.join(ROOT, "profiles", name)
+    import glob
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{cfg}_ncu_full.txt")), reverse=True)
+    cands += sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{cfg}_ncu_dram.txt")), reverse=True)
+    for p in cands:
         if not os.path.exists(p):
             continue
         for line in open(p):
