@@ -231,3 +231,33 @@ def test_host_pipeline_bitwise_equals_device_path(L, N, h, d, dt):
     assert fm.launch_count() >= 1
     assert np.array_equal(ho, o_dev.cpu().view(torch.int16).numpy())
     assert np.array_equal(hl, lse_dev.cpu().numpy())
+
+
+def test_pair_kernel_matches_single_cta_kernel_bitwise(oracle, tmp_path):
+    """d = 256: the CTA-pair kernel (cta_group::2, M = 256) and the single-CTA
+    kernel issue the same MMA K-order and the same softmax, so O and LSE are
+    bitwise equal.  The single-CTA path is forced in a subprocess
+    (FMHA_TUNE_PAIR=0 is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    import paper_2312_11918_b200 as fm
+    L, N, h, d = 1, 1152, 2, 256   # 9 Q tiles: the pair path pads the last unit
+    q, k, v = oracle.problem(L, N, h, d, 31, dtype="f16")
+    np.savez(tmp_path / "in.npz", q=q, k=k, v=v)
+    tq, tk, tv = (torch.from_numpy(x).cuda().half() for x in (q, k, v))
+    o, lse = fm.fmha_fwd(tq, tk, tv)
+    torch.cuda.synchronize()
+    code = (
+        "import numpy as np, torch, paper_2312_11918_b200 as fm\n"
+        f"z = np.load({str(tmp_path / 'in.npz')!r})\n"
+        "q, k, v = (torch.from_numpy(z[n]).cuda().half() for n in ('q', 'k', 'v'))\n"
+        "o, lse = fm.fmha_fwd(q, k, v)\n"
+        f"np.savez({str(tmp_path / 'out.npz')!r}, o=o.float().cpu().numpy(), lse=lse.cpu().numpy())\n")
+    env = dict(os.environ, FMHA_TUNE_PAIR="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=300)
+    ref = np.load(tmp_path / "out.npz")
+    np.testing.assert_array_equal(o.float().cpu().numpy(), ref["o"])
+    np.testing.assert_array_equal(lse.cpu().numpy(), ref["lse"])
