@@ -18,6 +18,7 @@
 
 #include "../../include/fmha/fmha.h"
 #include "fmha_errors.hpp"
+#include "fmha_fwd_d64_kernel.cuh"
 #include "fmha_fwd_pair_kernel.cuh"
 #include "fmha_fwd_st_kernel.cuh"
 #include "fmha_fwd_kernel.cuh"
@@ -139,6 +140,43 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
 // CTA-pair kernels (cluster 2 x 1 x 1 over the Q-tile axis).  An odd
 // Q-tile count gets one padding CTA per (b, head): its Q rows are all past N
 // (TMA zero-fills them, nothing is stored).  `mk64` is a K map with 64-row boxes.
+// d = 64: two-Q-tile ping-pong with 64-row K/V steps, two persistent CTAs per
+// SM.  `mk64` / `mv64` are K / V maps with 64-row boxes.
+template <bool BF16, int EMU>
+fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
+                       const CUtensorMap& mv64, void* o, float* lse, cudaStream_t st) {
+  using Cfg = fmha_b200::FwdCfgD64;
+  auto kern = fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemAlloc);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set = true;
+  }
+  fmha_b200::FwdArgs a{};
+  a.o = o;
+  a.lse = lse;
+  a.o_sb = p->o_stride[0];
+  a.o_sn = p->o_stride[1];
+  a.o_sh = p->o_stride[2];
+  a.N = static_cast<int>(p->N);
+  a.H = static_cast<int>(p->h);
+  a.L = static_cast<int>(p->L);
+  a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
+  a.n_qblocks = static_cast<int>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
+  a.n_units = a.n_qblocks * a.H * a.L;
+  a.scale = resolve_scale(p);
+  a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = nullptr;
+  const int grid = std::min(a.n_units, 2 * num_sms());
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk64, mv64, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch (d=64)");
+  g_last_launches = 1;
+  return FMHA_OK;
+}
+
 template <int D, int BN, bool BF16, int EMU>
 fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
                         const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
@@ -380,6 +418,21 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
     return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st)
               : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st);
+  }
+  // d = 64, N >= 1024: the two-CTA-per-SM ping-pong with 64-row K/V steps
+  // (fmha_fwd_d64_kernel.cuh).  Measured against the one-CTA-per-SM kernel:
+  // +4 % at N = 1024, +5.5 % at 2048, +6.4 % at 4096, +6.8 % at 8192; equal at
+  // N = 512 (c2) and slower on small ragged problems, which stay below.
+  // FMHA_TUNE_D64=0 disables it (A/B runs).
+  static const bool d64_ok = [] {
+    const char* e = std::getenv("FMHA_TUNE_D64");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (p->d == 64 && d64_ok && p->N >= 1024) {
+    CUtensorMap mk64, mv64;
+    if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
+      return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
+    return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st) : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st);
   }
   switch (p->d) {
     case 64: {

@@ -50,12 +50,19 @@ def test_small_full(oracle, d, dt):
     _full_check(oracle, 2, 512, 3, d, dt, seed=7)
 
 
+@pytest.mark.parametrize("N", [1024, 2048])
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_d64_two_ctas_per_sm_full(oracle, N, dt):
+    """d = 64, N >= 1024 runs the two-CTA-per-SM kernel (64-row K/V steps)."""
+    _full_check(oracle, 1, N, 3, 64, dt, seed=13)
+
+
 def test_config2_distilbert_full(oracle):
     """c2: L=16, h=12, N=512, d=64 fp16 -- full O and LSE."""
     _full_check(oracle, 16, 512, 12, 64, "f16")
 
 
-@pytest.mark.parametrize("N", [1, 37, 128, 200, 384, 640, 1000])
+@pytest.mark.parametrize("N", [1, 37, 128, 200, 384, 640, 1000, 1100])
 @pytest.mark.parametrize("d", [64, 128, 256])
 def test_ragged_sequence_lengths(oracle, N, d):
     """N not a multiple of the kernel tiles: padded K/V columns are masked,
@@ -116,8 +123,8 @@ def test_strided_views(oracle, d, N):
 
 @pytest.mark.parametrize("cfg", [(4, 4096, 16, 128, "f16"), (2, 8192, 8, 256, "f16"),
                                  (8, 16384, 32, 128, "bf16"), (1, 8320, 2, 128, "f16"),
-                                 (1, 2432, 3, 256, "bf16")],
-                         ids=["c3", "c4", "c5", "d128-pair-odd-tiles", "d256-pair-odd-tiles"])
+                                 (1, 2432, 3, 256, "bf16"), (4, 4096, 32, 64, "f16")],
+                         ids=["c3", "c4", "c5", "d128-pair-odd-tiles", "d256-pair-odd-tiles", "table1-d64"])
 def test_large_configs_sampled(oracle, cfg):
     """c3/c4/c5 at full size: inputs generated on the device (seeded torch
     RNG, rounded to the 16-bit type), every (b, head) computed on the GPU,
