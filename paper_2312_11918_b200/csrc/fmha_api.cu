@@ -108,7 +108,7 @@ int num_sms() {
 
 template <int D, bool BF16, int EMU = 0>
 fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
-                        const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st) {
+                        const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfg<D>;
   auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
   static bool attr_set = false;  // benign race: idempotent attribute set
@@ -121,10 +121,11 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   fmha_b200::FwdArgs a{};
   a.lse = lse;
   a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
   a.H = static_cast<int>(p->h);
   a.L = static_cast<int>(p->L);
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
-  a.n_qblocks = static_cast<int>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
+  a.n_qblocks = static_cast<int>((nq + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
   a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
@@ -144,7 +145,7 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
 // SM.  `mk64` / `mv64` are K / V maps with 64-row boxes.
 template <bool BF16, int EMU>
 fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
-                       const CUtensorMap& mv64, void* o, float* lse, cudaStream_t st) {
+                       const CUtensorMap& mv64, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgD64;
   auto kern = fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>;
   static bool attr_set = false;
@@ -161,10 +162,11 @@ fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CU
   a.o_sn = p->o_stride[1];
   a.o_sh = p->o_stride[2];
   a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
   a.H = static_cast<int>(p->h);
   a.L = static_cast<int>(p->L);
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
-  a.n_qblocks = static_cast<int>((p->N + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
+  a.n_qblocks = static_cast<int>((nq + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
   a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
@@ -179,7 +181,7 @@ fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CU
 
 template <int D, int BN, bool BF16, int EMU>
 fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
-                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgPair<D, BN>;
   auto kern = fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>;
   static bool attr_set = false;
@@ -196,13 +198,14 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.o_sn = p->o_stride[1];
   a.o_sh = p->o_stride[2];
   a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
   a.H = static_cast<int>(p->h);
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
   a.trace = nullptr;
   cudaLaunchConfig_t cfg{};
-  const unsigned n_qtiles = static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM);
+  const unsigned n_qtiles = static_cast<unsigned>((nq + Cfg::kBM - 1) / Cfg::kBM);
   cfg.gridDim = dim3((n_qtiles + 1) & ~1u, static_cast<unsigned>(p->h), static_cast<unsigned>(p->L));
   cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmemAlloc;
@@ -223,7 +226,7 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
 
 template <int D, bool BF16, int BN>
 fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
-                      const CUtensorMap& mv, void* o, float* lse, cudaStream_t st) {
+                      const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgST<D, BN>;
   auto kern = fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>;
   static bool attr_set = false;
@@ -240,12 +243,13 @@ fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUt
   a.o_sn = p->o_stride[1];
   a.o_sh = p->o_stride[2];
   a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
   a.H = static_cast<int>(p->h);
   a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
   a.trace = nullptr;
-  dim3 grid(static_cast<unsigned>((p->N + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
+  dim3 grid(static_cast<unsigned>((nq + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
             static_cast<unsigned>(p->L));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
@@ -327,6 +331,17 @@ cudaError_t copy_slice(char* dst, const char* src, const int64_t st[3], const fm
   return e;
 }
 
+// Copy query rows [n0, n1) of batch b (all heads) of a BSHD tensor between
+// host and device buffers that share the same layout.
+cudaError_t copy_rows(char* dst, const char* src, const int64_t st[3], const fmha_fwd_params* p, int64_t b,
+                      int64_t n0, int64_t n1, cudaMemcpyKind kind, cudaStream_t s) {
+  const size_t off = static_cast<size_t>(st[0] * b + st[1] * n0) * 2;
+  if (st[1] == p->h * p->d && st[2] == p->d)  // dense rows: one contiguous range
+    return cudaMemcpyAsync(dst + off, src + off, static_cast<size_t>((n1 - n0) * st[1]) * 2, kind, s);
+  return cudaMemcpy2DAsync(dst + off, static_cast<size_t>(st[1]) * 2, src + off, static_cast<size_t>(st[1]) * 2,
+                           static_cast<size_t>((p->h - 1) * st[2] + p->d) * 2, static_cast<size_t>(n1 - n0), kind, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -384,21 +399,27 @@ fmha_status fmha_fwd_check(const fmha_fwd_params* p) {
   return FMHA_OK;
 }
 
-fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, const void* v, void* o,
-                     float* lse, void* cuda_stream) {
+// fmha_fwd on the first `nq` query rows from `q` / `o` (keys and values: all
+// p->N rows; LSE rows at `lse` + row with row stride p->N).  nq == p->N is the
+// public entry point; the host pipeline also calls it on row slices of Q.
+static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void* k, const void* v, void* o,
+                            float* lse, void* cuda_stream, int64_t nq) {
   g_last_launches = 0;
   fmha_status s = fmha_fwd_check(p);
   if (s != FMHA_OK) return s;
+  if (nq < 1 || nq > p->N) return fail(FMHA_ERR_CONFIG, "query row count out of range");
+  fmha_fwd_params pq = *p;  // Q / O maps span the nq rows
+  pq.N = nq;
   if (!q || !k || !v || !o) return fail(FMHA_ERR_CONFIG, "null tensor pointer");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
     return fail(FMHA_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
   const int rows = 128;
   const int kv_rows = 128;  // K/V TMA box rows (d = 256 also streams 128-row K/V steps)
   CUtensorMap mq, mk, mv, mo;
-  if (!make_map(&mq, q, p->dtype, p, p->q_stride, rows) ||
+  if (!make_map(&mq, q, p->dtype, &pq, p->q_stride, rows) ||
       !make_map(&mk, k, p->dtype, p, p->k_stride, kv_rows) ||
       !make_map(&mv, v, p->dtype, p, p->v_stride, kv_rows) ||
-      !make_map(&mo, o, p->dtype, p, p->o_stride, rows))
+      !make_map(&mo, o, p->dtype, &pq, p->o_stride, rows))
     return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or arguments)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool bf = p->dtype == FMHA_BF16;
@@ -416,8 +437,8 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     CUtensorMap mkh, mvh;
     if (!make_map(&mkh, k, p->dtype, p, p->k_stride, 32) || !make_map(&mvh, v, p->dtype, p, p->v_stride, 64))
       return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
-    return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st)
-              : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st);
+    return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st, nq)
+              : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st, nq);
   }
   // d = 64, N >= 1024: the two-CTA-per-SM ping-pong with 64-row K/V steps
   // (fmha_fwd_d64_kernel.cuh).  Measured against the one-CTA-per-SM kernel:
@@ -432,7 +453,7 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
     CUtensorMap mk64, mv64;
     if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
       return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
-    return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st) : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st);
+    return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st, nq) : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st, nq);
   }
   switch (p->d) {
     case 64: {
@@ -446,16 +467,16 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
       }();
       const int emu64 = emu64_env >= 0 ? emu64_env : (p->N >= 1024 ? 6 : 4);
       if (emu64 == 0)
-        return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st, nq);
       if (emu64 == 6)
-        return bf ? launch_d128<64, true, 6>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 6>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<64, true, 6>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<64, false, 6>(p, mq, mk, mv, mo, lse, st, nq);
       if (emu64 == 8)
-        return bf ? launch_d128<64, true, 8>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<64, false, 8>(p, mq, mk, mv, mo, lse, st);
-      return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st)
-                : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<64, true, 8>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<64, false, 8>(p, mq, mk, mv, mo, lse, st, nq);
+      return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
+                : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }
     case 128: {
       // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default 4 of 16 pairs)
@@ -464,19 +485,19 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
         return e ? std::atoi(e) : 4;
       }();
       if (emu == 0)
-        return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st, nq);
       if (emu == 2)
-        return bf ? launch_d128<128, true, 2>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 2>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<128, true, 2>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<128, false, 2>(p, mq, mk, mv, mo, lse, st, nq);
       if (emu == 6)
-        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<128, true, 6>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<128, false, 6>(p, mq, mk, mv, mo, lse, st, nq);
       if (emu == 8)
-        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st)
-                  : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st);
-      return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st)
-                : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st);
+        return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st, nq);
+      return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
+                : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }
     default: {
       // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound).
@@ -486,12 +507,17 @@ fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, con
         CUtensorMap mk64;
         if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
           return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
-        return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st)
-                  : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st);
+        return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st, nq)
+                  : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st, nq);
       }
-      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st);
+      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st, nq) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st, nq);
     }
   }
+}
+
+fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, const void* v, void* o,
+                     float* lse, void* cuda_stream) {
+  return fwd_rows(p, q, k, v, o, lse, cuda_stream, p ? p->N : 0);
 }
 
 fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k, const void* v,
@@ -535,6 +561,14 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   const std::vector<InChunk> plan = plan_chunks(p, static_cast<size_t>(16) << 20, static_cast<size_t>(4) << 20);
   size_t n_ev = plan.size();
   for (const InChunk& c : plan) n_ev += c.groups.size();
+  // The last chunk, when it is one batch of a long sequence, is split by query
+  // rows: its K and V go first, then Q in row slices whose kernels and O / LSE
+  // copies start as each slice lands, so the work left after the final H2D
+  // byte is one slice instead of a whole batch.
+  const bool slice_last = plan.back().b1 - plan.back().b0 == 1 && p->N >= 1024;
+  const int64_t batch_out = p->N * p->h * p->d * 2;  // ~4 MB of O per slice, 2..16 slices
+  const int64_t kSlices = std::min<int64_t>(16, std::max<int64_t>(2, batch_out >> 22));
+  n_ev += slice_last ? 2 * kSlices : 0;
   while (ws.ev_in.size() < n_ev) {
     cudaEvent_t a;
     if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess)
@@ -543,8 +577,47 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   }
   int launches = 0;
   size_t ev = 0;
-  for (const InChunk& ic : plan) {
+  for (size_t ci = 0; ci < plan.size(); ++ci) {
+    const InChunk& ic = plan[ci];
     const Chunk all{ic.b0, ic.b1, 0, p->h};
+    if (slice_last && ci + 1 == plan.size()) {
+      const int64_t b = ic.b0;
+      if ((e = copy_slice(dk, static_cast<const char*>(k), p->k_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||
+          (e = copy_slice(dv, static_cast<const char*>(v), p->v_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpyAsync H2D");
+      fmha_fwd_params pc = *p;
+      pc.L = 1;
+      const int64_t step = ((p->N + kSlices - 1) / kSlices + 255) / 256 * 256;  // whole 256-row Q blocks
+      for (int64_t n0 = 0; n0 < p->N; n0 += step) {
+        const int64_t n1 = std::min(p->N, n0 + step);
+        cudaEvent_t in_done = ws.ev_in[ev++];
+        if ((e = copy_rows(dq, static_cast<const char*>(q), p->q_stride, p, b, n0, n1, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||
+            (e = cudaEventRecord(in_done, ws.s_in)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(ws.s_comp, in_done, 0)) != cudaSuccess)
+          return cuda_fail(e, "cudaMemcpyAsync H2D");
+        auto at = [&](char* base, const int64_t st[3], int64_t row) {
+          return base + static_cast<size_t>(st[0] * b + st[1] * row) * 2;
+        };
+        float* dl_c = dl ? dl + static_cast<size_t>(b * p->h * p->N + n0) : nullptr;
+        s = fwd_rows(&pc, at(dq, p->q_stride, n0), at(dk, p->k_stride, 0), at(dv, p->v_stride, 0),
+                     at(dO, p->o_stride, n0), dl_c, ws.s_comp, n1 - n0);
+        if (s != FMHA_OK) return s;
+        ++launches;
+        cudaEvent_t comp_done = ws.ev_in[ev++];
+        if ((e = cudaEventRecord(comp_done, ws.s_comp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(ws.s_out, comp_done, 0)) != cudaSuccess ||
+            (e = copy_rows(static_cast<char*>(o), dO, p->o_stride, p, b, n0, n1, cudaMemcpyDeviceToHost, ws.s_out)) != cudaSuccess)
+          return cuda_fail(e, "cudaMemcpyAsync D2H");
+        if (lse) {  // [h] rows of (n1 - n0) floats, pitch N
+          const size_t ol = static_cast<size_t>(b * p->h * p->N + n0);
+          if ((e = cudaMemcpy2DAsync(lse + ol, static_cast<size_t>(p->N) * 4, dl + ol, static_cast<size_t>(p->N) * 4,
+                                     static_cast<size_t>(n1 - n0) * 4, static_cast<size_t>(p->h),
+                                     cudaMemcpyDeviceToHost, ws.s_out)) != cudaSuccess)
+            return cuda_fail(e, "cudaMemcpyAsync D2H lse");
+        }
+      }
+      continue;
+    }
     cudaEvent_t in_done = ws.ev_in[ev++];
     if ((e = copy_slice(dq, static_cast<const char*>(q), p->q_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||
         (e = copy_slice(dk, static_cast<const char*>(k), p->k_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(320, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[q]);
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
-      if (row < N) {
+      if (row < args.n_q) {
         uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
                          static_cast<int64_t>(row) * args.o_sn + static_cast<int64_t>(head) * args.o_sh;
 #pragma unroll

@@ -63,7 +63,8 @@ struct FwdArgs {
   void* o;                   // BSHD output (direct-store epilogue of the d=256 kernel)
   int64_t o_sb, o_sn, o_sh;  // output strides (elements)
   float* lse;        // [L][h][N] fp32 or nullptr
-  int N, H, L;
+  int N, H, L;      // N: key/value length (and the LSE row stride)
+  int n_q;           // query rows from the Q/O base (N, or a host-pipeline row slice)
   int n_kv_tiles;    // ceil(N / kBN)
   int n_qblocks;     // Q blocks per head (256 rows for d<=128, 128 for d=256)
   int n_units;       // L * H * n_qblocks
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_arrive(stage_ready);   // this warp's 32 rows staged
       }
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
-      if (row < N && args.lse != nullptr)
+      if (row < args.n_q && args.lse != nullptr)
         args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
       trace_stamp(args, trq, q, n_kv - 1, 7);
 #ifdef FMHA_TRACE_BUILD

@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(192, FwdCfgPair<D_, kBN_>::kCtasPerSm)
     mbar_wait(o_full, 0);
     tc_fence_after();
     const int row = qrow0 + r;
-    const bool row_ok = row < N;
+    const bool row_ok = row < args.n_q;
     const float inv = 1.0f / l;
     uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
                      static_cast<int64_t>(row_ok ? row : 0) * args.o_sn +

@@ -219,11 +219,14 @@ def test_launch_count():
     (2, 4096, 16, 128, "f16"),   # 1 batch per input chunk, O/LSE returned in 4 head groups (2-D copies)
     (8, 512, 8, 64, "bf16"),     # several batches per input chunk
     (3, 2048, 6, 256, "f16"),    # d=256 kernel behind the pipeline
+    (2, 2048, 4, 64, "f16"),     # last batch split into query-row slices (d=64 kernel)
+    (1, 1100, 3, 128, "bf16"),   # row slices with a ragged last slice
 ])
 def test_host_pipeline_bitwise_equals_device_path(L, N, h, d, dt):
     """fmha_fwd_host splits the problem into (batch, head-group) chunks over
-    three streams; every chunk is an independent sub-problem, so the result
-    must equal the single-launch device path bit for bit."""
+    three streams, and the last batch of a long sequence into query-row
+    slices; every chunk is an independent sub-problem, so the result must
+    equal the single-launch device path bit for bit."""
     import torch
     import paper_2312_11918_b200 as fm
     td = torch.bfloat16 if dt == "bf16" else torch.float16
