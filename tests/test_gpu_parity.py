@@ -100,7 +100,7 @@ def test_custom_scale(oracle):
     _full_check(oracle, 1, 256, 2, 128, "f16", scale=0.05)
 
 
-@pytest.mark.parametrize("d,N", [(128, 384), (256, 512)], ids=["d128", "d256-pair"])
+@pytest.mark.parametrize("d,N", [(128, 384), (256, 512), (64, 1024)], ids=["d128", "d256-pair", "d64-two-ctas"])
 def test_strided_views(oracle, d, N):
     """Q/K/V as views into one packed (L, N, 3, h, d) buffer and O into a
     padded buffer: the ABI's explicit strides (head-sharding path, 8(e)).
