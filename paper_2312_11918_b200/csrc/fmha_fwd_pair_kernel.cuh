@@ -5,9 +5,9 @@
 // Same contract as the other forward kernels (fmhasim::fmha_forward,
 // /root/reference/proj/src/attention.cpp:153-173); same per-CTA structure as
 // fmha_fwd_st_kernel.cuh (one 128-row Q tile per CTA, double-buffered S in
-// TMEM, 128-row K/V steps), but the two CTAs of a 2-CTA cluster -- adjacent
-// Q tiles of one (b, head) -- run every GEMM as ONE M = 256 tcgen05.mma
-// issued by the leader CTA:
+// TMEM), but the two CTAs of a 2-CTA cluster -- adjacent Q tiles of one
+// (b, head) -- run every GEMM as ONE M = 256 tcgen05.mma issued by the
+// leader CTA (shown for d = 256, kBN = 128):
 //
 //   S = Q K^T   M256 N128 K256: A = each CTA's own Q tile, B = K tile split
 //               by kv rows: CTA r holds K rows [64r, 64r+64) (32 KB);
@@ -17,16 +17,19 @@
 // Each SM therefore streams HALF of every K/V tile (64 KB per 128-row step
 // instead of 128 KB) -- at d = 256 the single-CTA kernel is bound by the
 // chip's L2 -> SM delivery rate (profiles/r01_microbench.txt) -- and the
-// 32 KB half-tiles make a 5-slot ring in the same shared memory (vs 2 x 64 KB).
+// half-tiles make a deeper ring in the same shared memory (5 x 32 KB vs
+// 2 x 64 KB).  At d = 128, kBN = 64: M256 N64 S GEMMs, M256 N128 PV GEMMs,
+// 8 KB half-tiles in an 8-slot ring, TMEM 256 columns per CTA.
 //
 // Protocol (mbarriers; "L" = lives in the leader CTA only):
-//   bar_q  L  both CTAs' Q TMA complete on it (128 KB expected by the leader)
-//   kv_full[s] L  both halves of slot s (64 KB expected by the leader)
+//   bar_q  L  both CTAs' Q TMA complete on it (two Q tiles expected)
+//   kv_full[s] L  both halves of slot s
 //   kv_empty[s]  per CTA; the leader's MMA commit arrives in both CTAs
 //   s_full[2], pv_done, o_full  per CTA; multicast commits from the leader
 //   p_full[2] L  one arrival per softmax warp of BOTH CTAs (count 8)
 // Only the leader's MMA warp issues; the peer's MMA warp just co-allocates
-// TMEM.  Launch: cluster (2,1,1) over the Q-tile axis, tile count even.
+// TMEM.  Launch: cluster (2,1,1) over the Q-tile axis; an odd Q-tile count
+// is padded with one tile past N (zero-filled by TMA, nothing stored).
 #pragma once
 
 #include <cuda.h>
