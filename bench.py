@@ -309,6 +309,7 @@ def run_ours(args):
             "data": "synthetic: device-side seeded N(0,1) rounded to the 16-bit type",
             "config": {"workload": cfg["desc"], "L": global_L, "h": h, "N": N, "d": d, "causal": False,
                        "per_gpu_L": L, "parallelism": f"batch-shard x{world} (no collective)",
+                       "kernel": fm.kernel_for(L, N, h, d, cfg["dtype"]),
                        "l2": ("inputs %.0f MB per GPU > 126 MB L2" % (work_bytes / 2 ** 20)) if flush is None
                        else "L2 flushed (256 MB write) between timed steps"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

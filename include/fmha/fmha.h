@@ -127,6 +127,11 @@ fmha_status fmha_tensor_load(const char* path, float* data, int64_t count);
 /* 4 * N^2 * d * h * L (attention_flops, attention.cpp:191-193). */
 int64_t fmha_attention_flops(int64_t L, int64_t N, int64_t h, int64_t d);
 
+/* Name of the kernel fmha_fwd would launch for this problem (host-only, no
+ * CUDA call; NULL when fmha_fwd_check rejects the parameters).  The choice
+ * depends on d and N (and on FMHA_TUNE_* environment overrides). */
+const char* fmha_kernel_for(const fmha_fwd_params* p);
+
 /* Number of kernel launches the last fmha_fwd call on this thread issued. */
 int fmha_last_launch_count(void);
 

@@ -74,6 +74,8 @@ def lib():
         L.fmha_attention_flops.restype = C.c_int64
         L.fmha_last_error.restype = C.c_char_p
         L.fmha_last_launch_count.restype = C.c_int
+        L.fmha_kernel_for.argtypes = [P]
+        L.fmha_kernel_for.restype = C.c_char_p
         L.fmha_version.restype = C.c_char_p
         L.fmha_host_f32_to_16.argtypes = [C.c_float, C.c_int]
         L.fmha_host_f32_to_16.restype = C.c_uint16
@@ -246,6 +248,16 @@ def fmha_fwd_reference(q, k, v, scale=None):
 
 
 CLI_PATH = os.path.join(HERE, "fmha-b200")
+
+
+def kernel_for(L, N, h, d, dtype=F16) -> str:
+    """Name of the kernel fmha_fwd launches for a dense (L, N, h, d) problem
+    (host-only query of the dispatcher)."""
+    p = dense_params(L, N, h, d, _dtype_code(dtype) if isinstance(dtype, str) else dtype)
+    name = lib().fmha_kernel_for(C.byref(p))
+    if name is None:
+        _raise(lib().fmha_fwd_check(C.byref(p)))
+    return name.decode()
 
 
 def launch_count() -> int:

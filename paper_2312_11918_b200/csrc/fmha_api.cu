@@ -342,6 +342,60 @@ cudaError_t copy_rows(char* dst, const char* src, const int64_t st[3], const fmh
                            static_cast<size_t>((p->h - 1) * st[2] + p->d) * 2, static_cast<size_t>(n1 - n0), kind, s);
 }
 
+// ------------------------------------------------------- kernel choice --
+// Environment overrides for A/B tuning runs, read once per process:
+//   FMHA_TUNE_PAIR=0   no CTA-pair kernels;  FMHA_TUNE_D64=0  no two-CTA d=64
+//   kernel;  FMHA_TUNE_EMU / FMHA_TUNE_EMU64  exp2 split of the ping-pong kernel.
+struct Tuning {
+  bool pair_ok, d64_ok;
+  int emu64, emu128;
+};
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    auto env = [](const char* n, int dflt) {
+      const char* e = std::getenv(n);
+      return e ? std::atoi(e) : dflt;
+    };
+    return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
+                  env("FMHA_TUNE_EMU", 4)};
+  }();
+  return t;
+}
+
+enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kPair128, kPair256, kSingle256 };
+
+// Which kernel runs a (valid) problem; thresholds are measured crossovers
+// (profiles/r01_microbench.txt):
+//  * d = 128, N >= 8192: CTA pairs with one Q tile per CTA and 64-column
+//    double-buffered S, two CTAs per SM (+2 % at N = 8192, +3.5 % at 16384,
+//    +6 % on c5; -1 % at 4096 and -5..-10 % below, where the persistent
+//    ping-pong kernel's unit loop beats the per-CTA prologue / epilogue);
+//  * d = 64, N >= 1024: the two-CTA-per-SM ping-pong with 64-row K/V steps
+//    (+4 % at N = 1024 .. +6.8 % at 8192; equal at 512, slower on small
+//    ragged problems);
+//  * d = 256, N > 128: CTA pairs (M = 256 MMAs, each SM streams half of every
+//    K/V tile; a single Q tile would pay a whole padding CTA);
+//  * otherwise the persistent ping-pong kernel (d <= 128) or the single-CTA
+//    d = 256 kernel.
+Kernel select_kernel(const fmha_fwd_params* p) {
+  const Tuning& t = tuning();
+  if (p->d == 64) return t.d64_ok && p->N >= 1024 ? Kernel::kD64TwoCta : Kernel::kPingPong64;
+  if (p->d == 128) return t.pair_ok && p->N >= 8192 ? Kernel::kPair128 : Kernel::kPingPong128;
+  return t.pair_ok && p->N > 128 ? Kernel::kPair256 : Kernel::kSingle256;
+}
+
+const char* kernel_name(Kernel k) {
+  switch (k) {
+    case Kernel::kPingPong64: return "fmha_fwd_sm100_kernel<64> (persistent two-Q-tile ping-pong)";
+    case Kernel::kD64TwoCta: return "fmha_fwd_d64_kernel (ping-pong, 64-row K/V steps, two CTAs per SM)";
+    case Kernel::kPingPong128: return "fmha_fwd_sm100_kernel<128> (persistent two-Q-tile ping-pong)";
+    case Kernel::kPair128: return "fmha_fwd_pair_kernel<128,64> (CTA pairs, two CTAs per SM)";
+    case Kernel::kPair256: return "fmha_fwd_pair_kernel<256,128> (CTA pairs)";
+    case Kernel::kSingle256: return "fmha_fwd_st_kernel<256,128> (single CTA)";
+  }
+  return "";
+}
+
 }  // namespace
 
 extern "C" {
@@ -423,49 +477,23 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
     return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or arguments)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool bf = p->dtype == FMHA_BF16;
-  // FMHA_TUNE_PAIR=0 keeps every head dim off the CTA-pair kernels (A/B runs)
-  static const bool pair_ok = [] {
-    const char* e = std::getenv("FMHA_TUNE_PAIR");
-    return !(e && std::atoi(e) == 0);
-  }();
-  // d = 128, long sequences: one Q tile per CTA with double-buffered 64-column
-  // S (no S -> softmax -> PV chain), two CTAs per SM, CTA pairs sharing K/V.
-  // Measured against the persistent ping-pong kernel: +2 % at N = 8192, +3.5 %
-  // at 16384 (+6 % on c5); -1 % at 4096 and -5..-10 % below (per-CTA prologue
-  // and epilogue of the non-persistent grid), so shorter sequences stay there.
-  if (p->d == 128 && pair_ok && p->N >= 8192) {
-    CUtensorMap mkh, mvh;
-    if (!make_map(&mkh, k, p->dtype, p, p->k_stride, 32) || !make_map(&mvh, v, p->dtype, p, p->v_stride, 64))
-      return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
-    return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st, nq)
-              : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st, nq);
-  }
-  // d = 64, N >= 1024: the two-CTA-per-SM ping-pong with 64-row K/V steps
-  // (fmha_fwd_d64_kernel.cuh).  Measured against the one-CTA-per-SM kernel:
-  // +4 % at N = 1024, +5.5 % at 2048, +6.4 % at 4096, +6.8 % at 8192; equal at
-  // N = 512 (c2) and slower on small ragged problems, which stay below.
-  // FMHA_TUNE_D64=0 disables it (A/B runs).
-  static const bool d64_ok = [] {
-    const char* e = std::getenv("FMHA_TUNE_D64");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (p->d == 64 && d64_ok && p->N >= 1024) {
-    CUtensorMap mk64, mv64;
-    if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
-      return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
-    return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st, nq) : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st, nq);
-  }
-  switch (p->d) {
-    case 64: {
-      // exp2 split (pairs of 16 on the polynomial): at d=64 the tensor core
-      // has slack, so long sequences move more exponentials to the FMA pipe
-      // (6/16: L=4,h=32,N=4096 686 -> 730 TFLOP/s); short ones keep 4/16.
-      // FMHA_TUNE_EMU64 overrides for tuning runs.
-      static const int emu64_env = [] {
-        const char* e = std::getenv("FMHA_TUNE_EMU64");
-        return e ? std::atoi(e) : -1;
-      }();
-      const int emu64 = emu64_env >= 0 ? emu64_env : (p->N >= 1024 ? 6 : 4);
+  switch (select_kernel(p)) {
+    case Kernel::kPair128: {
+      CUtensorMap mkh, mvh;
+      if (!make_map(&mkh, k, p->dtype, p, p->k_stride, 32) || !make_map(&mvh, v, p->dtype, p, p->v_stride, 64))
+        return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
+      return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st, nq)
+                : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st, nq);
+    }
+    case Kernel::kD64TwoCta: {
+      CUtensorMap mk64, mv64;
+      if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
+        return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
+      return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st, nq)
+                : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st, nq);
+    }
+    case Kernel::kPingPong64: {
+      const int emu64 = tuning().emu64 >= 0 ? tuning().emu64 : (p->N >= 1024 ? 6 : 4);
       if (emu64 == 0)
         return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
                   : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st, nq);
@@ -478,12 +506,8 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       return bf ? launch_d128<64, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
                 : launch_d128<64, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }
-    case 128: {
-      // FMHA_TUNE_EMU selects the exp2 split for tuning runs (default 4 of 16 pairs)
-      static const int emu = [] {
-        const char* e = std::getenv("FMHA_TUNE_EMU");
-        return e ? std::atoi(e) : 4;
-      }();
+    case Kernel::kPingPong128: {
+      const int emu = tuning().emu128;
       if (emu == 0)
         return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
                   : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st, nq);
@@ -499,25 +523,28 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }
-    default: {
-      // CTA pairs halve the K/V bytes each SM streams (the d = 256 bound).
-      // They pair adjacent Q tiles; a single Q tile (N <= 128) would pay a
-      // whole padding CTA, so it stays on the single-CTA kernel.
-      if (pair_ok && p->N > 128) {
-        CUtensorMap mk64;
-        if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
-          return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
-        return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st, nq)
-                  : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st, nq);
-      }
-      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st, nq) : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st, nq);
+    case Kernel::kPair256: {
+      CUtensorMap mk64;
+      if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
+        return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
+      return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st, nq)
+                : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st, nq);
     }
+    case Kernel::kSingle256:
+    default:
+      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st, nq)
+                : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st, nq);
   }
 }
 
 fmha_status fmha_fwd(const fmha_fwd_params* p, const void* q, const void* k, const void* v, void* o,
                      float* lse, void* cuda_stream) {
   return fwd_rows(p, q, k, v, o, lse, cuda_stream, p ? p->N : 0);
+}
+
+const char* fmha_kernel_for(const fmha_fwd_params* p) {
+  if (fmha_fwd_check(p) != FMHA_OK) return nullptr;
+  return kernel_name(select_kernel(p));
 }
 
 fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k, const void* v,
