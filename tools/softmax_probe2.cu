@@ -10,6 +10,8 @@
 //       polynomial with the MUFU stream instead of hoisting it
 //   V3  V2 + MUFU inputs of the next group depending on the polynomial
 //       result (strict alternation)
+//   V4  the d=128 pair kernel's 64-column tile (x64 load, 64 exps, one x32
+//       store), 1-4 warps per sub-partition (clk per 64-column tile)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -maxrregcount=168 \
 //        -I paper_2312_11918_b200/csrc tools/softmax_probe2.cu -o build/softmax_probe2
 #include <cuda_runtime.h>
@@ -61,7 +63,7 @@ __device__ __forceinline__ float exp_rowsum_pack_il(const float (&s)[128], float
 }
 
 template <int V>
-__global__ void __launch_bounds__(256, 1) probe(int iters, float zero, long long* clk, float* sink) {
+__global__ void __launch_bounds__(V == 4 ? 512 : 256, 1) probe(int iters, float zero, long long* clk, float* sink) {
   __shared__ uint32_t tmem_holder;
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc(&tmem_holder, 512);
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(256, 1) probe(int iters, float zero, long long
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_holder;
-  const uint32_t base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * 256;
+  const uint32_t base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + (warp >> 2) * (V == 4 ? 128 : 256);
   {  // fill S with scores in [-4, 4)
     uint32_t v[32];
     for (int c = 0; c < 4; ++c) {
@@ -84,6 +86,27 @@ __global__ void __launch_bounds__(256, 1) probe(int iters, float zero, long long
   __syncthreads();
   const long long c0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if constexpr (V == 4) {  // the d=128 pair kernel's 64-column tile
+      uint32_t sr[64];
+      tmem_ld32x32b_x64(base, sr);
+      float s[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(sr[c]);
+      float mx[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
+#pragma unroll
+      for (int c = 16; c < 64; c += 16)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
+      const float m = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      uint32_t p0[32];
+      l += exp_rowsum_pack<false, 0, 64, 2>(s, 0.1275f, -m * 0.1275f, p0);
+      tmem_st32x32b_x32(base + 64, p0);
+      tmem_wait_st();
+      __syncwarp();
+      continue;
+    }
     uint32_t sr[128];
     tmem_ld32x32b_x128(base, sr);
     float s[128];
@@ -121,7 +144,7 @@ __global__ void __launch_bounds__(256, 1) probe(int iters, float zero, long long
     __syncwarp();
   }
   const long long c1 = clock64();
-  if ((threadIdx.x & 31) == 0) clk[blockIdx.x * 8 + warp] = c1 - c0;
+  if ((threadIdx.x & 31) == 0) clk[blockIdx.x * 16 + warp] = c1 - c0;
   sink[blockIdx.x * blockDim.x + threadIdx.x] = l;
   tc_fence_before();
   __syncthreads();
@@ -133,8 +156,8 @@ template <int V>
 void run(int threads) {
   long long* clk;
   float* sink;
-  cudaMalloc(&clk, 148 * 8 * 8);
-  cudaMalloc(&sink, 148 * 256 * 4);
+  cudaMalloc(&clk, 148 * 16 * 8);
+  cudaMalloc(&sink, 148 * 512 * 4);
   const int iters = 2000;
   probe<V><<<148, threads>>>(10, 0.f, clk, sink);
   probe<V><<<148, threads>>>(iters, 0.f, clk, sink);
@@ -142,7 +165,7 @@ void run(int threads) {
     printf("V%d failed\n", V);
     return;
   }
-  long long c[8];
+  long long c[16];
   cudaMemcpy(c, clk, sizeof(c), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int w = 0; w < threads / 32; ++w) avg += c[w];
@@ -158,6 +181,9 @@ int main() {
     run<1>(t);
     run<2>(t);
     run<3>(t);
+    run<4>(t);
   }
+  run<4>(384);  // three warps per SMSP
+  run<4>(512);
   return 0;
 }
