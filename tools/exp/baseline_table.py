@@ -11,8 +11,8 @@ for c in ("c1", "c2", "c3", "c4", "c5"):
     j = json.load(open(f"profiles/{tag}_bench_{c}.json"))
     r = j["roofline"]
     e = j["e2e"]
-    k = json.load(open("profiles/ncu_summary.json")).get(c, {}).get("kernel", "")
-    k = k.split("(")[0].replace("void ", "").replace("fmha_b200::", "")
+    k = j["config"].get("kernel") or json.load(open("profiles/ncu_summary.json")).get(c, {}).get("kernel", "")
+    k = k.replace("void ", "").replace("fmha_b200::", "")
     ck = j["clocks"]
     clk = f"{ck['sm_mhz']} MHz {' '.join(ck['reasons'])}".strip()
     print(f"| {names[c]} | {j['n_gpus']} | {j['dtype']} | {j['ms_per_step']:.4f} ms | {j['value']:.1f} | "
