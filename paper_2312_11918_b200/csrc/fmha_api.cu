@@ -493,7 +493,8 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
                 : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st, nq);
     }
     case Kernel::kPingPong64: {
-      const int emu64 = tuning().emu64 >= 0 ? tuning().emu64 : (p->N >= 1024 ? 6 : 4);
+      // exp2 split 6/16 (measured: +1 % over 4/16 at N = 512 / 768, equal at 256)
+      const int emu64 = tuning().emu64 >= 0 ? tuning().emu64 : 6;
       if (emu64 == 0)
         return bf ? launch_d128<64, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
                   : launch_d128<64, false, 0>(p, mq, mk, mv, mo, lse, st, nq);
