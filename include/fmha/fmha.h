@@ -124,6 +124,13 @@ fmha_status fmha_tensor_save(const char* path, const float* data, int64_t L, int
 fmha_status fmha_tensor_load_header(const char* path, int64_t dims[4], int* f16);
 fmha_status fmha_tensor_load(const char* path, float* data, int64_t count);
 
+/* Host quantisers used by fmha_forward_f32 (threaded; F16C when the CPU has it):
+ * float -> fp16 with the reference's semantics (half.hpp:12-42: round to nearest
+ * even, finite overflow saturates to +-65504, subnormals kept) or -> bf16 (RNE),
+ * and back.  Bit-identical to an element-wise loop. */
+void fmha_host_quantize(const float* src, uint16_t* dst, int64_t n, fmha_dtype dtype);
+void fmha_host_dequantize(const uint16_t* src, float* dst, int64_t n, fmha_dtype dtype);
+
 /* 4 * N^2 * d * h * L (attention_flops, attention.cpp:191-193). */
 int64_t fmha_attention_flops(int64_t L, int64_t N, int64_t h, int64_t d);
 

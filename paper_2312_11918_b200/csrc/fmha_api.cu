@@ -550,6 +550,14 @@ const char* fmha_kernel_for(const fmha_fwd_params* p) {
 
 fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k, const void* v,
                           void* o, float* lse, int device) {
+  return fmha_b200::fwd_host_pipeline(p, q, k, v, o, lse, device, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q, const void* k, const void* v,
+                                         void* o, float* lse, int device,
+                                         void (*prepare)(void*, int64_t, int64_t), void* ctx) {
   fmha_status s = fmha_fwd_check(p);
   if (s != FMHA_OK) return s;
   if (!q || !k || !v || !o) return fail(FMHA_ERR_CONFIG, "null tensor pointer");
@@ -608,6 +616,7 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   for (size_t ci = 0; ci < plan.size(); ++ci) {
     const InChunk& ic = plan[ci];
     const Chunk all{ic.b0, ic.b1, 0, p->h};
+    if (prepare) prepare(ctx, ic.b0, ic.b1);
     if (slice_last && ci + 1 == plan.size()) {
       const int64_t b = ic.b0;
       if ((e = copy_slice(dk, static_cast<const char*>(k), p->k_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||
@@ -685,5 +694,3 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
   if ((e = cudaStreamSynchronize(ws.s_out)) != cudaSuccess) return cuda_fail(e, "kernel execution");
   return FMHA_OK;
 }
-
-}  // extern "C"

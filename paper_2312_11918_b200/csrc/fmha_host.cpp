@@ -2,12 +2,19 @@
 // the fmha_forward_f32 C entry point, and the C++ drop-in adapter
 // (include/fmha/fmha.hpp) mirroring fmhasim::fmha_forward
 // (/root/reference/proj/include/fmhasim/attention.hpp:58-59).
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "../../include/fmha/fmha.h"
 #include "../../include/fmha/fmha.hpp"
@@ -95,22 +102,75 @@ void parallel_for(int64_t n, F&& fn) {
   for (auto& x : th) x.join();
 }
 
+#if defined(__x86_64__)
+// F16C fast paths (8 values per instruction).  vcvtps2ph with round-to-nearest
+// -even equals f32_to_f16_sat for every |x| <= 65504 (subnormal results
+// included); groups of 8 holding a NaN or a larger magnitude take the scalar
+// path, which saturates finite values and keeps inf / canonical NaN.
+__attribute__((target("avx2,f16c"))) void to_f16_f16c(const float* src, uint16_t* dst, int64_t a, int64_t b) {
+  const __m256 lim = _mm256_set1_ps(65504.0f);
+  const __m256 abs_mask = _mm256_castsi256_ps(_mm256_set1_epi32(0x7FFFFFFF));
+  int64_t i = a;
+  for (; i + 8 <= b; i += 8) {
+    const __m256 x = _mm256_loadu_ps(src + i);
+    const __m256 special = _mm256_cmp_ps(_mm256_and_ps(x, abs_mask), lim, _CMP_NLE_UQ);  // > lim or NaN
+    if (_mm256_movemask_ps(special)) {
+      for (int t = 0; t < 8; ++t) dst[i + t] = f32_to_f16_sat(src[i + t]);
+      continue;
+    }
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(dst + i), _mm256_cvtps_ph(x, _MM_FROUND_TO_NEAREST_INT));
+  }
+  for (; i < b; ++i) dst[i] = f32_to_f16_sat(src[i]);
+}
+__attribute__((target("avx2,f16c"))) void from_f16_f16c(const uint16_t* src, float* dst, int64_t a, int64_t b) {
+  int64_t i = a;
+  for (; i + 8 <= b; i += 8)
+    _mm256_storeu_ps(dst + i, _mm256_cvtph_ps(_mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i))));
+  for (; i < b; ++i) dst[i] = f16_to_f32(src[i]);
+}
+bool has_f16c() {
+  static const bool ok = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("f16c");
+  return ok;
+}
+#endif
+
 void to_16(const float* src, uint16_t* dst, int64_t n, fmha_dtype dt) {
   parallel_for(n, [&](int64_t a, int64_t b) {
-    if (dt == FMHA_BF16)
+    if (dt == FMHA_BF16) {
       for (int64_t i = a; i < b; ++i) dst[i] = f32_to_bf16(src[i]);
-    else
-      for (int64_t i = a; i < b; ++i) dst[i] = f32_to_f16_sat(src[i]);
+      return;
+    }
+#if defined(__x86_64__)
+    if (has_f16c()) return to_f16_f16c(src, dst, a, b);
+#endif
+    for (int64_t i = a; i < b; ++i) dst[i] = f32_to_f16_sat(src[i]);
   });
 }
 
 void from_16(const uint16_t* src, float* dst, int64_t n, fmha_dtype dt) {
   parallel_for(n, [&](int64_t a, int64_t b) {
-    if (dt == FMHA_BF16)
+    if (dt == FMHA_BF16) {
       for (int64_t i = a; i < b; ++i) dst[i] = bf16_to_f32(src[i]);
-    else
-      for (int64_t i = a; i < b; ++i) dst[i] = f16_to_f32(src[i]);
+      return;
+    }
+#if defined(__x86_64__)
+    if (has_f16c()) return from_f16_f16c(src, dst, a, b);
+#endif
+    for (int64_t i = a; i < b; ++i) dst[i] = f16_to_f32(src[i]);
   });
+}
+
+// Pinned 16-bit staging for fmha_forward_f32 (Q, K, V, O), kept across calls:
+// page-locked buffers let fmha_fwd_host's copies run at the full PCIe rate and
+// overlap its kernels; pageable vectors would be staged by the driver.
+struct Staging {
+  std::mutex mu;
+  uint16_t* buf = nullptr;
+  size_t elems = 0;
+};
+Staging& staging() {
+  static Staging s;
+  return s;
 }
 
 }  // namespace
@@ -121,6 +181,13 @@ uint16_t fmha_host_f32_to_16(float x, int bf16) {
   return bf16 ? f32_to_bf16(x) : f32_to_f16_sat(x);
 }
 float fmha_host_16_to_f32(uint16_t x, int bf16) { return bf16 ? bf16_to_f32(x) : f16_to_f32(x); }
+
+void fmha_host_quantize(const float* src, uint16_t* dst, int64_t n, fmha_dtype dtype) {
+  if (src && dst && n > 0) to_16(src, dst, n, dtype);
+}
+void fmha_host_dequantize(const uint16_t* src, float* dst, int64_t n, fmha_dtype dtype) {
+  if (src && dst && n > 0) from_16(src, dst, n, dtype);
+}
 
 fmha_status fmha_forward_f32(const float* q, const float* k, const float* v, int64_t L, int64_t N,
                              int64_t h, int64_t d, int64_t bM, int64_t bN, fmha_dtype dtype,
@@ -140,13 +207,46 @@ fmha_status fmha_forward_f32(const float* q, const float* k, const float* v, int
     return FMHA_ERR_CONFIG;
   }
   const int64_t n = L * N * h * d;
-  std::vector<uint16_t> hq(n), hk(n), hv(n), ho(n);
-  to_16(q, hq.data(), n, dtype);
-  to_16(k, hk.data(), n, dtype);
-  to_16(v, hv.data(), n, dtype);
-  s = fmha_fwd_host(&p, hq.data(), hk.data(), hv.data(), ho.data(), lse, device);
+  Staging& stg = staging();
+  std::lock_guard<std::mutex> lock(stg.mu);
+  std::vector<uint16_t> pageable;  // fallback when page-locked memory is unavailable
+  uint16_t* base = nullptr;
+  if (stg.elems >= static_cast<size_t>(4 * n)) {
+    base = stg.buf;
+  } else {
+    if (stg.buf) cudaFreeHost(stg.buf);
+    stg.buf = nullptr;
+    stg.elems = 0;
+    void* b = nullptr;
+    if (cudaHostAlloc(&b, static_cast<size_t>(4 * n) * 2, cudaHostAllocPortable) == cudaSuccess) {
+      stg.buf = static_cast<uint16_t*>(b);
+      stg.elems = static_cast<size_t>(4 * n);
+      base = stg.buf;
+    } else {
+      cudaGetLastError();  // clear the allocation error, use pageable memory
+      pageable.resize(static_cast<size_t>(4 * n));
+      base = pageable.data();
+    }
+  }
+  uint16_t *hq = base, *hk = base + n, *hv = base + 2 * n, *ho = base + 3 * n;
+  // quantise each input chunk just before the pipeline copies it, so the
+  // conversion of chunk c+1 overlaps the copies / kernels of chunk c
+  struct Ctx {
+    const float *q, *k, *v;
+    uint16_t *hq, *hk, *hv;
+    int64_t per_batch;
+    fmha_dtype dt;
+  } ctx{q, k, v, hq, hk, hv, N * h * d, dtype};
+  auto prepare = [](void* c, int64_t b0, int64_t b1) {
+    const Ctx& x = *static_cast<const Ctx*>(c);
+    const int64_t off = b0 * x.per_batch, cnt = (b1 - b0) * x.per_batch;
+    to_16(x.q + off, x.hq + off, cnt, x.dt);
+    to_16(x.k + off, x.hk + off, cnt, x.dt);
+    to_16(x.v + off, x.hv + off, cnt, x.dt);
+  };
+  s = fmha_b200::fwd_host_pipeline(&p, hq, hk, hv, ho, lse, device, prepare, &ctx);
   if (s != FMHA_OK) return s;
-  from_16(ho.data(), o, n, dtype);
+  from_16(ho, o, n, dtype);
   return FMHA_OK;
 }
 

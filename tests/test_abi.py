@@ -115,6 +115,31 @@ def test_host_f16_conversion_matches_reference_quantiser(oracle):
     assert (nan16 & 0x7C00) == 0x7C00 and (nan16 & 0x3FF) != 0
 
 
+def test_bulk_quantiser_matches_elementwise(oracle):
+    """fmha_host_quantize / dequantize (threaded, F16C fast path) are bit-identical
+    to the reference quantiser on ordinary values and on every special case
+    (saturation band, inf, NaN, subnormals), including odd lengths and tails."""
+    import ctypes as C
+    lib = fm.lib()
+    lib.fmha_host_quantize.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
+    lib.fmha_host_dequantize.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([rng.standard_normal(300001) * s for s in (1e-7, 1e-4, 1, 3e4, 1e5)]).astype(np.float32)
+    special = np.array([65504, 65519.99, 65520, -65520, 7e4, np.inf, -np.inf, np.nan, 2 ** -24, 2 ** -25,
+                        1.5 * 2 ** -25, -0.0, 2 ** -14 * (1 - 2 ** -12)], np.float32)
+    xs[rng.integers(0, xs.size, 5000)] = rng.choice(special, 5000)
+    for dt, code in (("f16", fm.F16), ("bf16", fm.BF16)):
+        got = np.empty(xs.size, np.uint16)
+        lib.fmha_host_quantize(xs.ctypes.data, got.ctypes.data, xs.size, code)
+        ref = oracle.to_bits(xs, dt)
+        nan = np.isnan(xs)
+        np.testing.assert_array_equal(got[~nan], ref[~nan])
+        assert np.all((got[nan] & 0x7F80 if dt == "bf16" else got[nan] & 0x7C00) > 0)
+        back = np.empty(xs.size, np.float32)
+        lib.fmha_host_dequantize(got.ctypes.data, back.ctypes.data, xs.size, code)
+        np.testing.assert_array_equal(back[~nan], oracle.from_bits(got, dt)[~nan])
+
+
 def test_cpp_adapter_header_compiles(tmp_path):
     """The C++ drop-in adapter header (fmha.hpp) compiles against a reference-style caller."""
     import shutil
