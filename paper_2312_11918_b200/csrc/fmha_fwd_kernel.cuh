@@ -111,8 +111,14 @@ struct FwdCfg {
   static constexpr int kStoreWarp = 10;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kSeqBar = 1;  // named barriers 1, 2: exponential-phase turns of WG 0, 1
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
+
+#ifndef FMHA_SEQ
+#define FMHA_SEQ 0
+#endif
+constexpr bool kSeq = FMHA_SEQ != 0;
 
 // unit -> (b, head, q-block)
 __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int& head, int& qb) {
@@ -173,13 +179,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&s_full[q], 1);
-      for (int c = 0; c < C::kPChunks; ++c) mbar_init(&p_full[q * C::kPChunks + c], 4);  // one per softmax warp
+      for (int c = 0; c < C::kPChunks; ++c) mbar_init(&p_full[q * C::kPChunks + c], 128);  // every softmax thread
       mbar_init(&o_full[q], 1);
-      mbar_init(&o_empty[q], 4);
+      mbar_init(&o_empty[q], 128);
     }
     mbar_init(&stage_free[0], 1);
     mbar_init(&stage_free[1], 1);
-    mbar_init(stage_ready, 4);
+    mbar_init(stage_ready, 128);
     fence_mbar_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
@@ -382,6 +388,12 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tO = tmem + lane_off + (q ? C::kColO1 : C::kColO0);
     const float sl2 = args.scale_log2;
     const int N = args.N;
+    // shared-window barrier addresses, computed once (hot loop)
+    const uint32_t a_s_full = smem_u32(&s_full[q]);
+    const uint32_t a_p_full0 = smem_u32(&p_full[q * 2]), a_p_full1 = smem_u32(&p_full[q * 2 + 1]);
+    // WG 0 takes the first turn of the exponential phases
+    if constexpr (kSeq)
+      if (q == 1) named_bar_arrive(C::kSeqBar, 256);
     uint32_t it = 0;
     int i = 0;
     for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(384, 1)
       float l = 0.0f;       // running sum of exp2((s - m) * sl2)
 
       for (int j = 0; j < n_kv; ++j, ++it) {
-        mbar_wait(&s_full[q], it & 1);
+        mbar_wait_addr(a_s_full, it & 1);
         trace_stamp(args, trq, q, j, 0);
 #ifdef FMHA_TRACE_BUILD
         if (tr && i < 8 && r == 0 && j == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 1 + q] = clock64();
@@ -416,12 +428,12 @@ __global__ void __launch_bounds__(384, 1)
           const float alpha = ex2_approx((m - m_new) * sl2);
           l *= alpha;
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32x32b_x32(tO + c * 32, o);
+          for (int c = 0; c < D / 16; ++c) {  // x16 chunks: S stays in registers meanwhile
+            uint32_t o[16];
+            tmem_ld32x32b_x16(tO + c * 16, o);
 #pragma unroll
-            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tmem_st32x32b_x32(tO + c * 32, o);
+            for (int t = 0; t < 16; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tmem_st32x32b_x16(tO + c * 16, o);
           }
           m = m_new;
         };
@@ -460,18 +472,24 @@ __global__ void __launch_bounds__(384, 1)
         const float neg = -m * sl2;
         const bool masked = valid < C::kBN;
         uint32_t p0[32], p1[32];
+        // The exponential phases of the two WGs run in strict turns (named
+        // barriers kSeqBar + q): each gets the sub-partitions' MUFU / FMA
+        // pipes alone instead of both slowing down when their phases overlap.
+        if constexpr (kSeq) named_bar_sync(C::kSeqBar + q, 256);
         float rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
                           : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
         trace_stamp(args, trq, q, j, 9);
         tmem_st32x32b_x32(tS, p0);
         rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
                      : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        if constexpr (kSeq) named_bar_arrive(C::kSeqBar + (q ^ 1), 256);
         trace_stamp(args, trq, q, j, 10);
+        // every thread arrives once its own TMEM stores have completed (no
+        // lane-0 branch, no warp reconvergence on the critical path)
         auto publish = [&](int half) {
           tmem_wait_st();
           tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[q * 2 + half]);
+          mbar_arrive_addr(half ? a_p_full1 : a_p_full0);
         };
         publish(0);
         trace_stamp(args, trq, q, j, 2);
@@ -520,11 +538,8 @@ __global__ void __launch_bounds__(384, 1)
       }
       tc_fence_before();
       fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&o_empty[q]);   // O_q drained from TMEM
-        mbar_arrive(stage_ready);   // this warp's 32 rows staged
-      }
+      mbar_arrive(&o_empty[q]);  // O_q drained from TMEM (all 128 threads)
+      mbar_arrive(stage_ready);  // this thread's row staged
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
       if (row < args.n_q && args.lse != nullptr)
         args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
@@ -533,6 +548,9 @@ __global__ void __launch_bounds__(384, 1)
       if (tr && i < 8 && r == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 3 + q] = clock64();
 #endif
     }
+    // consume WG 1's last hand-over so no named barrier is left half-arrived
+    if constexpr (kSeq)
+      if (q == 0) named_bar_sync(C::kSeqBar, 256);
   }
 
   tc_fence_before();

@@ -79,6 +79,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Variants on a precomputed shared-window address (hot loops: the generic ->
+// shared conversion of the dynamic-smem base is then done once per kernel).
+__device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
+  if (mbar_try_wait(a, parity)) return;
+#ifndef FMHA_NO_WATCHDOG
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait(a, parity)) {
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
+#else
+  while (!mbar_try_wait(a, parity)) {
+  }
+#endif
+}
+__device__ __forceinline__ void mbar_arrive_addr(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+
 // Spin variant for a warp with nothing else to do that sits on the critical
 // path (the MMA issuer): non-blocking test_wait, no hardware suspend.
 __device__ __forceinline__ uint32_t mbar_test_wait(uint32_t addr, uint32_t parity) {
@@ -352,6 +370,9 @@ __device__ __forceinline__ void st_shared_v4(void* ptr, uint32_t a, uint32_t b, 
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace fmha_b200
