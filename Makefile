@@ -30,6 +30,12 @@ trace: build/libfmha_b200_trace.so
 build/libfmha_b200_trace.so: $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh | build
 	$(NVCC) $(NVFLAGS) -DFMHA_TRACE_BUILD -shared -o $@ $(SRCS) -lpthread 2> build/ptxas_trace.log || (cat build/ptxas_trace.log; false)
 
+# watchdog build (mbarrier waits trap after ~4 s): tests of risky kernel changes,
+# tools/sanitize_smoke.py; FMHA_B200_LIB=build/libfmha_b200_watchdog.so selects it
+watchdog: build/libfmha_b200_watchdog.so
+build/libfmha_b200_watchdog.so: $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh | build
+	$(NVCC) $(NVFLAGS) -DFMHA_WATCHDOG -shared -o $@ $(SRCS) -lpthread 2> build/ptxas_watchdog.log || (cat build/ptxas_watchdog.log; false)
+
 oracle:
 	$(MAKE) -s -C oracle all
 
@@ -43,4 +49,4 @@ clean:
 	rm -f $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean trace
+.PHONY: all oracle clean trace watchdog

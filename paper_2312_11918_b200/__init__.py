@@ -166,21 +166,30 @@ def fmha_fwd(q, k, v, o=None, lse=None, scale=None, stream=None, want_lse=True):
         raise ValueError("q/k/v dtypes differ")
     if not (q.shape == k.shape == v.shape) or q.dim() != 4:
         raise ValueError("AttentionProblem: Q/K/V shape mismatch")
+    dev = q.device
+    if dev.type != "cuda" or k.device != dev or v.device != dev:
+        raise ValueError("q/k/v must be CUDA tensors on one device")
     L, N, h, d = q.shape
     if o is None:
         o = torch.empty_like(q, memory_format=torch.contiguous_format)
+    elif o.shape != q.shape or o.dtype != q.dtype or o.device != dev:
+        raise ValueError(f"o must be a {q.dtype} tensor of shape {tuple(q.shape)} on {dev}")
     if lse is None and want_lse:
-        lse = torch.empty((L, h, N), dtype=torch.float32, device=q.device)
+        lse = torch.empty((L, h, N), dtype=torch.float32, device=dev)
+    elif lse is not None and (lse.shape != (L, h, N) or lse.dtype != torch.float32 or lse.device != dev
+                              or not lse.is_contiguous()):
+        raise ValueError(f"lse must be a contiguous float32 tensor of shape {(L, h, N)} on {dev}")
     p = FwdParams()
     p.L, p.N, p.h, p.d = L, N, h, d
     p.q_stride, p.k_stride, p.v_stride, p.o_stride = (_strides(q, "q"), _strides(k, "k"),
                                                       _strides(v, "v"), _strides(o, "o"))
     p.scale = float(scale or 0.0)
     p.dtype = BF16 if q.dtype == torch.bfloat16 else F16
-    if stream is None:
-        stream = torch.cuda.current_stream(q.device)
-    st = lib().fmha_fwd(C.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                        lse.data_ptr() if lse is not None else None, stream.cuda_stream)
+    with torch.cuda.device(dev):  # launch on q's device (the ABI uses the current one)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        st = lib().fmha_fwd(C.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                            lse.data_ptr() if lse is not None else None, stream.cuda_stream)
     if st:
         _raise(st)
     return o, lse

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -97,13 +98,40 @@ unsigned long long* trace_buffer(size_t n) {
   return buf;
 }
 
+// SM count of the current device (cached per device: one process may drive
+// several GPUs through the host entry points).
 int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
-  }();
+  }
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
   return n;
+}
+
+// The >48 KB dynamic shared memory opt-in of kernel K on the current device.
+// The attribute belongs to the device context, so it is applied once per
+// (kernel, device) -- not once per process.
+template <auto K>
+cudaError_t ensure_smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};  // bit d: set on device d
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = (dev >= 0 && dev < 64) ? (1ull << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 template <int D, bool BF16, int EMU = 0>
@@ -111,13 +139,8 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
                         const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfg<D>;
   auto kern = fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>;
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::kSmemAlloc);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_sm100_kernel<D, BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
   fmha_b200::FwdArgs a{};
   a.lse = lse;
   a.N = static_cast<int>(p->N);
@@ -148,13 +171,8 @@ fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CU
                        const CUtensorMap& mv64, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgD64;
   auto kern = fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::kSmemAlloc);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
   fmha_b200::FwdArgs a{};
   a.o = o;
   a.lse = lse;
@@ -184,13 +202,8 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
                         const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgPair<D, BN>;
   auto kern = fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::kSmemAlloc);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
   fmha_b200::FwdArgs a{};
   a.o = o;
   a.lse = lse;
@@ -229,13 +242,8 @@ fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUt
                       const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
   using Cfg = fmha_b200::FwdCfgST<D, BN>;
   auto kern = fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::kSmemAlloc);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>>(Cfg::kSmemAlloc); e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
   fmha_b200::FwdArgs a{};
   a.o = o;
   a.lse = lse;
@@ -561,18 +569,45 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   fmha_status s = fmha_fwd_check(p);
   if (s != FMHA_OK) return s;
   if (!q || !k || !v || !o) return fail(FMHA_ERR_CONFIG, "null tensor pointer");
-  // Host buffers are taken as BSHD of the strides given (elements spanned =
-  // stride[0] * L); the device copies use the same layout.
-  const size_t nq = static_cast<size_t>(p->q_stride[0] * p->L) * 2;
-  const size_t nk = static_cast<size_t>(p->k_stride[0] * p->L) * 2;
-  const size_t nv = static_cast<size_t>(p->v_stride[0] * p->L) * 2;
-  const size_t no = static_cast<size_t>(p->o_stride[0] * p->L) * 2;
+  // Host buffers are BSHD views of the strides given; the device copies use
+  // the same layout, so each region must be batch-major and non-overlapping
+  // (the chunked copies move whole batches / row ranges of it).
+  const int64_t* all_st[4] = {p->q_stride, p->k_stride, p->v_stride, p->o_stride};
+  for (const int64_t* st : all_st)
+    if (st[2] < p->d || st[1] < (p->h - 1) * st[2] + p->d || st[0] < (p->N - 1) * st[1] + (p->h - 1) * st[2] + p->d)
+      return fail(FMHA_ERR_CONFIG,
+                  "host entry point: strides must describe a batch-major, non-overlapping BSHD layout "
+                  "(stride[2] >= d, stride[1] >= (h-1)*stride[2]+d, stride[0] >= (N-1)*stride[1]+(h-1)*stride[2]+d)");
+  // elements spanned by a view: the last element's offset + 1
+  auto extent = [&](const int64_t st[3]) {
+    return static_cast<size_t>((p->L - 1) * st[0] + (p->N - 1) * st[1] + (p->h - 1) * st[2] + p->d) * 2;
+  };
+  const size_t nq = extent(p->q_stride);
+  const size_t nk = extent(p->k_stride);
+  const size_t nv = extent(p->v_stride);
+  const size_t no = extent(p->o_stride);
   const size_t nl = lse ? static_cast<size_t>(p->L * p->h * p->N) * 4 : 0;
   auto up = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
   const size_t total = up(nq) + up(nk) + up(nv) + up(no) + up(nl);
   Workspace& ws = workspace(device);
   std::lock_guard<std::mutex> lock(ws.mu);
-  cudaError_t e = cudaSetDevice(device);
+  // Restores the caller's current device on every exit, and on an error exit
+  // drains the three streams first so no queued copy still touches the
+  // caller's host buffers (or the shared staging) after this call returns.
+  struct Guard {
+    Workspace& ws;
+    int prev = -1;
+    bool ok = false;
+    ~Guard() {
+      if (!ok)
+        for (cudaStream_t st : {ws.s_in, ws.s_comp, ws.s_out})
+          if (st) cudaStreamSynchronize(st);
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } guard{ws};
+  cudaError_t e = cudaGetDevice(&guard.prev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   for (cudaStream_t* st : {&ws.s_in, &ws.s_comp, &ws.s_out})
     if (!*st && (e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking)) != cudaSuccess)
@@ -692,5 +727,6 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   }
   g_last_launches = launches;
   if ((e = cudaStreamSynchronize(ws.s_out)) != cudaSuccess) return cuda_fail(e, "kernel execution");
+  guard.ok = true;
   return FMHA_OK;
 }

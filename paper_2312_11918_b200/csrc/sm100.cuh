@@ -55,14 +55,17 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// Wait for the phase with the given parity to complete.  The watchdog
-// (default on; -DFMHA_NO_WATCHDOG removes it) traps after ~4 s instead of
-// hanging the GPU, so a protocol bug surfaces as a launch error, not a dead
-// box.  -DFMHA_WATCHDOG_PRINTF adds a diagnostic line (costs registers).
+// Wait for the phase with the given parity to complete.  The watchdog is
+// opt-in (-DFMHA_WATCHDOG: test / debug builds such as `make watchdog`): it
+// traps after ~4 s instead of hanging the GPU, so a protocol bug surfaces as a
+// launch error, not a dead box.  Production builds leave it out -- a trap is a
+// sticky error that poisons the caller's whole CUDA context, and legitimate
+// waits can exceed any fixed bound under preemption, MPS time-slicing or a
+// debugger.  -DFMHA_WATCHDOG_PRINTF adds a diagnostic line (costs registers).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
-#ifndef FMHA_NO_WATCHDOG
+#ifdef FMHA_WATCHDOG
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) {
@@ -83,7 +86,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // shared conversion of the dynamic-smem base is then done once per kernel).
 __device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
   if (mbar_try_wait(a, parity)) return;
-#ifndef FMHA_NO_WATCHDOG
+#ifdef FMHA_WATCHDOG
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
@@ -113,7 +116,7 @@ __device__ __forceinline__ uint32_t mbar_test_wait(uint32_t addr, uint32_t parit
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_test_wait(a, parity)) return;
-#ifndef FMHA_NO_WATCHDOG
+#ifdef FMHA_WATCHDOG
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_test_wait(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();

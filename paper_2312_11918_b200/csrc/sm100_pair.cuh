@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t mbar_try_wait_cluster(uint32_t addr, uint32_
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait_cluster(a, parity)) return;
-#ifndef FMHA_NO_WATCHDOG
+#ifdef FMHA_WATCHDOG
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait_cluster(a, parity)) {
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
