@@ -15,7 +15,7 @@ import bench  # noqa: E402
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "1", "--ref-seconds", "2"], capture_output=True, text=True, timeout=600,
+                          "--warmup", "1", "--ref-seconds", "2", "--config", "c1"], capture_output=True, text=True, timeout=600,
                          cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -25,6 +25,18 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "TFLOP/s"
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["gpu_launches"] == 0
+    assert "cpu_model" in line["cpu_baseline"]
+    # the same `config` object as the GPU arm prints (the driver compares them)
+    cfg, _, _, global_l = bench.workload("c1", 1, 0)
+    assert line["config"] == bench.config_dict(cfg, global_l)
+
+
+def test_reference_arm_rank_nonzero_is_silent():
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--config", "c1"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 0 and out.stdout.strip() == ""
 
 
 def test_workload_split():
