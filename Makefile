@@ -30,6 +30,11 @@ trace: build/libfmha_b200_trace.so
 build/libfmha_b200_trace.so: $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh | build
 	$(NVCC) $(NVFLAGS) -DFMHA_TRACE_BUILD -shared -o $@ $(SRCS) -lpthread 2> build/ptxas_trace.log || (cat build/ptxas_trace.log; false)
 
+# phase-profile build for tools/prof_phases.py (FMHA_B200_LIB selects it)
+prof: build/libfmha_b200_prof.so
+build/libfmha_b200_prof.so: $(SRCS) $(HDRS) $(PKG)/csrc/tmem_ops.cuh | build
+	$(NVCC) $(NVFLAGS) -DFMHA_PROF_BUILD -shared -o $@ $(SRCS) -lpthread 2> build/ptxas_prof.log || (cat build/ptxas_prof.log; false)
+
 # watchdog build (mbarrier waits trap after ~4 s): tests of risky kernel changes,
 # tools/sanitize_smoke.py; FMHA_B200_LIB=build/libfmha_b200_watchdog.so selects it
 watchdog: build/libfmha_b200_watchdog.so
@@ -49,4 +54,4 @@ clean:
 	rm -f $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean trace watchdog
+.PHONY: all oracle clean trace watchdog prof

@@ -23,6 +23,7 @@
 #include "fmha_fwd_pair_kernel.cuh"
 #include "fmha_fwd_st_kernel.cuh"
 #include "fmha_fwd_kernel.cuh"
+#include "fmha_fwd_split_kernel.cuh"
 
 namespace {
 
@@ -152,11 +153,42 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   a.n_units = a.n_qblocks * a.H * a.L;
   a.scale = resolve_scale(p);
   a.scale_log2 = a.scale * 1.4426950408889634f;
-  a.trace = trace_buffer(static_cast<size_t>(3 * a.n_kv_tiles * 16 + 64));
   const int grid = std::min(a.n_units, num_sms());
+  a.trace = trace_buffer(std::max<size_t>(static_cast<size_t>(3 * a.n_kv_tiles * 16 + 64),
+                                          static_cast<size_t>(grid) * 16 * 8));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  g_last_launches = 1;
+  return FMHA_OK;
+}
+
+// The split-row ping-pong kernel (two warps per softmax row): same unit /
+// grid as launch_d128.
+template <int D, bool BF16, int EMU>
+fmha_status launch_split(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
+                         const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st, int64_t nq) {
+  using Cfg = fmha_b200::SplitCfg<D>;
+  auto kern = fmha_b200::fmha_fwd_split_kernel<D, BF16, EMU>;
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_split_kernel<D, BF16, EMU>>(Cfg::kSmemAlloc);
+      e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
+  fmha_b200::FwdArgs a{};
+  a.lse = lse;
+  a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
+  a.H = static_cast<int>(p->h);
+  a.L = static_cast<int>(p->L);
+  a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
+  a.n_qblocks = static_cast<int>((nq + 2 * Cfg::kBM - 1) / (2 * Cfg::kBM));
+  a.n_units = a.n_qblocks * a.H * a.L;
+  a.scale = resolve_scale(p);
+  a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = nullptr;
+  const int grid = std::min(a.n_units, num_sms());
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch (split-row)");
   g_last_launches = 1;
   return FMHA_OK;
 }
@@ -357,6 +389,7 @@ cudaError_t copy_rows(char* dst, const char* src, const int64_t st[3], const fmh
 struct Tuning {
   bool pair_ok, d64_ok;
   int emu64, emu128;
+  int split;  // split-row ping-pong for d <= 128 (FMHA_TUNE_SPLIT)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -365,7 +398,7 @@ const Tuning& tuning() {
       return e ? std::atoi(e) : dflt;
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
-                  env("FMHA_TUNE_EMU", 4)};
+                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0)};
   }();
   return t;
 }
@@ -517,6 +550,16 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
     }
     case Kernel::kPingPong128: {
       const int emu = tuning().emu128;
+      if (tuning().split) {
+        if (emu == 2)
+          return bf ? launch_split<128, true, 2>(p, mq, mk, mv, mo, lse, st, nq)
+                    : launch_split<128, false, 2>(p, mq, mk, mv, mo, lse, st, nq);
+        if (emu == 6)
+          return bf ? launch_split<128, true, 6>(p, mq, mk, mv, mo, lse, st, nq)
+                    : launch_split<128, false, 6>(p, mq, mk, mv, mo, lse, st, nq);
+        return bf ? launch_split<128, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_split<128, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
+      }
       if (emu == 0)
         return bf ? launch_d128<128, true, 0>(p, mq, mk, mv, mo, lse, st, nq)
                   : launch_d128<128, false, 0>(p, mq, mk, mv, mo, lse, st, nq);

@@ -88,6 +88,42 @@ __device__ __forceinline__ void trace_stamp(const FwdArgs& a, bool on, int q, in
 #endif
 }
 
+// Phase profile (-DFMHA_PROF_BUILD, tools/prof_phases.py): every warp adds
+// the clock64 time since its previous mark to accumulator k, and writes the
+// totals to trace[(blockIdx.x * 16 + warp) * 8 + k] at exit.  Compiled out
+// otherwise.
+struct Prof {
+#ifdef FMHA_PROF_BUILD
+  unsigned long long acc[8];
+  long long last;
+  static __device__ __forceinline__ long long now() {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+  }
+  __device__ __forceinline__ Prof() : last(now()) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0;
+  }
+  __device__ __forceinline__ void mark(int k) {
+    const long long t = now();
+    acc[k] += static_cast<unsigned long long>(t - last);
+    last = t;
+  }
+  __device__ __forceinline__ void flush(const FwdArgs& a, int warp) {
+    if ((threadIdx.x & 31) == 0 && a.trace != nullptr)
+      for (int k = 0; k < 8; ++k) a.trace[(static_cast<size_t>(blockIdx.x) * 16 + warp) * 8 + k] = acc[k];
+  }
+#else
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(const FwdArgs&, int) {}
+#endif
+};
+
+#ifndef FMHA_O_IN_Q
+#define FMHA_O_IN_Q 0
+#endif
+
 template <int D>
 struct FwdCfg {
   static_assert(D == 64 || D == 128, "this kernel handles head dim 64 and 128");
@@ -96,13 +132,20 @@ struct FwdCfg {
   static constexpr int kChunks = D / 64;  // 128-B swizzle atoms along d
   static constexpr int kQTileBytes = kBM * D * 2;
   static constexpr int kKVTileBytes = kBN * D * 2;
-  static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
+  // FMHA_O_IN_Q=1 (d = 128, measured, not the default): O_q is staged for its
+  // TMA store in Q_q's own buffer (free once the unit's last S GEMMs are done;
+  // the next unit's Q load waits for both stores to be read), which buys a
+  // fifth 32 KB K/V slot.  The MMA warp's K/V waits did not shrink (272 vs
+  // 273 clk per period, tools/prof_phases.py) while every unit transition
+  // gained a Q-reload bubble: c3 1201 vs 1221 TFLOP/s, N=1024 -12 %.
+  static constexpr bool kOInQ = D == 128 && FMHA_O_IN_Q != 0;
+  static constexpr int kStages = D == 64 ? 8 : (kOInQ ? 5 : 4);  // K/V ring depth
   static constexpr int kQStages = D == 64 ? 2 : 1;  // Q double-buffered when it fits
   static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
-  static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both Q tiles
+  static constexpr int kSmemO = kOInQ ? 0 : kQTileBytes;  // epilogue staging, shared by both Q tiles
   static constexpr int kSmemRing = kStages * kKVTileBytes;
   static constexpr int kPChunks = 2;  // P published in two halves of 64 kv rows
-  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 7;
+  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 8;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
   static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
@@ -119,6 +162,13 @@ struct FwdCfg {
 #define FMHA_SEQ 0
 #endif
 constexpr bool kSeq = FMHA_SEQ != 0;
+#ifndef FMHA_SPEC
+#define FMHA_SPEC 0
+#endif
+constexpr bool kSpec = FMHA_SPEC != 0;  // speculative first half (see the softmax loop)
+#ifndef FMHA_KV_PREFETCH
+#define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
+#endif
 
 // unit -> (b, head, q-block)
 __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int& head, int& qb) {
@@ -153,8 +203,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* o_full = p_full + 2 * C::kPChunks;  // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
   uint64_t* stage_free = o_empty + 2;        // [2]: WG q's use of the O staging tile read by its TMA store
-  uint64_t* stage_ready = stage_free + 2;    // O staging tile written by a softmax WG
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 1);
+  uint64_t* stage_ready = stage_free + 2;    // [2] O_q staged by softmax WG q (kOInQ: one per WG)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -171,7 +221,8 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kQStages; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
+      // kOInQ: the last S GEMMs' commit + the read-out of both O stores
+      mbar_init(&q_empty[s], C::kOInQ ? 3 : 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&kv_full[s], 1);
@@ -185,7 +236,8 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_init(&stage_free[0], 1);
     mbar_init(&stage_free[1], 1);
-    mbar_init(stage_ready, 128);
+    mbar_init(&stage_ready[0], 128);
+    mbar_init(&stage_ready[1], 128);
     fence_mbar_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
@@ -217,6 +269,7 @@ __global__ void __launch_bounds__(384, 1)
         int slot = 0;
         uint32_t phase = 0;
         int i = 0;
+        Prof prof;
         for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
           int b, head, qb;
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
@@ -235,9 +288,20 @@ __global__ void __launch_bounds__(384, 1)
               tma_load_4d_hint(&tmQ, &q_full[qs], sQs + q * C::kQTileBytes + c * C::kBM * 128,
                                c * 64, head, qrow0 + q * C::kBM, b, once);
           for (int j = 0; j < n_kv; ++j) {
+#if FMHA_KV_PREFETCH > 0
+            // L2 prefetch of the K/V tiles FMHA_KV_PREFETCH steps ahead
+            if (j + FMHA_KV_PREFETCH < n_kv)
+#pragma unroll
+              for (int c = 0; c < C::kChunks; ++c) {
+                tma_prefetch_4d(&tmK, c * 64, head, (j + FMHA_KV_PREFETCH) * C::kBN, b);
+                tma_prefetch_4d(&tmV, c * 64, head, (j + FMHA_KV_PREFETCH) * C::kBN, b);
+              }
+#endif
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
+              prof.mark(3);
               mbar_wait(&kv_empty[slot], phase ^ 1);
+              prof.mark(0);
               mbar_arrive_expect_tx(&kv_full[slot], C::kKVTileBytes);
               uint8_t* dst = sRing + slot * C::kKVTileBytes;
 #pragma unroll
@@ -251,6 +315,8 @@ __global__ void __launch_bounds__(384, 1)
             }
           }
         }
+        prof.mark(3);
+        prof.flush(args, warp);
       }
     } else if (warp == C::kMmaWarp) {
       // ---------------------------------------------------- MMA issuer --
@@ -261,9 +327,13 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t ring_addr = smem_u32(sRing);
       int slot = 0;
       uint32_t phase = 0;
+      Prof prof;
+      int jj = 0;  // K/V tile index within the unit (profile only)
       auto next_slot = [&]() -> int {
         const int s = slot;
+        prof.mark(3);
         mbar_wait(&kv_full[s], phase);
+        prof.mark(jj < 2 ? 5 : 0);
         if (++slot == C::kStages) {
           slot = 0;
           phase ^= 1;
@@ -294,7 +364,13 @@ __global__ void __launch_bounds__(384, 1)
         constexpr int kStepsPerChunk = 8 / C::kPChunks;
 #pragma unroll
         for (int c = 0; c < C::kPChunks; ++c) {
+          prof.mark(3);
+#ifdef FMHA_SPIN_P
+          mbar_wait_spin(&p_full[q * C::kPChunks + c], par);
+#else
           mbar_wait(&p_full[q * C::kPChunks + c], par);
+#endif
+          prof.mark(1);
           if (c == C::kPChunks - 1) trace_stamp(args, trp, q, jt, 11);
           tc_fence_after();
 #pragma unroll
@@ -311,12 +387,15 @@ __global__ void __launch_bounds__(384, 1)
         const bool trm = tr && i == 0;
         const uint32_t ue = (static_cast<uint32_t>(i) & 1) ^ 1;  // o_empty parity
         const int qs = i % C::kQStages;
+        prof.mark(3);
         mbar_wait(&q_full[qs], static_cast<uint32_t>(i / C::kQStages) & 1);
+        prof.mark(4);
 #ifdef FMHA_TRACE_BUILD
         // per-unit timeline of CTA 0 (units 0..7): trace[(3*n_kv)*16 + i*8 + k]
         if (tr && i < 8) args.trace[(3 * n_kv) * 16 + i * 8 + 0] = clock64();
 #endif
         sQ_addr = smem_u32(sQ) + qs * 2 * C::kQTileBytes;
+        jj = 0;
         int ks = next_slot();
         tc_fence_after();
         mma_qk(0, ks);
@@ -326,16 +405,25 @@ __global__ void __launch_bounds__(384, 1)
         if (n_kv == 1) mma_commit_elect(&q_empty[qs]);
         mma_commit_elect(&kv_empty[ks]);
         for (int j = 1; j < n_kv; ++j) {
+          jj = j;
           const int vs = next_slot();
           ks = next_slot();
           const uint32_t par = it & 1;
-          if (j == 1) mbar_wait(&o_empty[0], ue);  // previous unit's epilogue drained O0
+          if (j == 1) {  // previous unit's epilogue drained O0
+            prof.mark(3);
+            mbar_wait(&o_empty[0], ue);
+            prof.mark(2);
+          }
           mma_pv(0, vs, j > 1, par, trm, j - 1);
           trace_stamp(args, trm, 0, j - 1, 12);
           mma_qk(0, ks);
           mma_commit_elect(&s_full[0]);
           trace_stamp(args, trm, 0, j - 1, 5);
-          if (j == 1) mbar_wait(&o_empty[1], ue);
+          if (j == 1) {
+            prof.mark(3);
+            mbar_wait(&o_empty[1], ue);
+            prof.mark(2);
+          }
           mma_pv(1, vs, j > 1, par, trm, j - 1);
           trace_stamp(args, trm, 1, j - 1, 12);
           mma_qk(1, ks);
@@ -357,22 +445,29 @@ __global__ void __launch_bounds__(384, 1)
         mma_commit_elect(&kv_empty[vs]);
         ++it;
       }
+      prof.mark(3);
+      prof.flush(args, warp);
     } else if (warp == C::kStoreWarp) {
       // ------------------------------------------------- O store warp --
       // Uses of the staging tile alternate WG0, WG1 per unit: use k = 2i+q.
+      // kOInQ: O_q sits in Q_q's buffer; once both stores of the unit have
+      // been read out, the Q stage is released to the producer (q_empty).
       if (lane == 0) {
         uint32_t k = 0;
-        for (int u = blockIdx.x; u < args.n_units; u += gridDim.x) {
+        int i = 0;
+        for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
           int b, head, qb;
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+          const int qs = i % C::kQStages;
           for (int q = 0; q < 2; ++q, ++k) {
-            mbar_wait(stage_ready, k & 1);
+            const uint8_t* src = C::kOInQ ? sQ + (qs * 2 + q) * C::kQTileBytes : sO;
+            mbar_wait(&stage_ready[C::kOInQ ? q : 0], C::kOInQ ? (static_cast<uint32_t>(i) & 1) : (k & 1));
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
-              tma_store_4d(&tmO, sO + c * C::kBM * 128, c * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
+              tma_store_4d(&tmO, src + c * C::kBM * 128, c * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
             tma_store_commit();
             tma_store_wait_read();
-            mbar_arrive(&stage_free[q]);
+            mbar_arrive(C::kOInQ ? &q_empty[qs] : &stage_free[q]);
           }
         }
         tma_store_wait_all();
@@ -396,6 +491,7 @@ __global__ void __launch_bounds__(384, 1)
       if (q == 1) named_bar_arrive(C::kSeqBar, 256);
     uint32_t it = 0;
     int i = 0;
+    Prof prof;
     for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
       int b, head, qb;
       decode_unit(u, args.n_qblocks, args.H, b, head, qb);
@@ -404,7 +500,14 @@ __global__ void __launch_bounds__(384, 1)
       float l = 0.0f;       // running sum of exp2((s - m) * sl2)
 
       for (int j = 0; j < n_kv; ++j, ++it) {
+        prof.mark(7);
+#ifdef FMHA_SPIN_S
+        while (!mbar_test_wait(a_s_full, it & 1)) {
+        }
+#else
         mbar_wait_addr(a_s_full, it & 1);
+#endif
+        prof.mark(0);
         trace_stamp(args, trq, q, j, 0);
 #ifdef FMHA_TRACE_BUILD
         if (tr && i < 8 && r == 0 && j == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 1 + q] = clock64();
@@ -422,6 +525,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int c = 0; c < 128; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
+        prof.mark(1);
         // Rescale O_q (TMEM) and the running sum by 2^((m - m_new) c); only
         // called while O_q is quiescent (S_q(j) observed => PV_q(j-1) done).
         auto rescale = [&](float m_new) {
@@ -449,10 +553,35 @@ __global__ void __launch_bounds__(384, 1)
           return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         };
+        // P half h = scores [64h, 64h+64) -> packed TMEM columns [32h, 32h+32)
+        // of S_q (S is already in registers).  Padded tiles take an all-MUFU
+        // copy (exact zeros for -inf scores).  The TMEM store of half 0 is
+        // waited for only after half 1's exponentials: the ~200-clk store
+        // latency leaves the critical path; GEMM-II on half 0 then overlaps
+        // the store and publication of half 1.
+        //
         // Conditional rescale (exact, since the final (m, Sigma) pair is
         // consistent): a warp keeps its stale max unless some row's max grew
-        // by more than 8 in log2 units (P stays <= 256).
-        {
+        // by more than 8 in log2 units (P stays <= 256).  After the first
+        // tile, half 0 is exponentiated speculatively against the stale max
+        // while the new row max is reduced in the same instruction stream;
+        // only when a row's max grew by more than 8 is the half redone.
+        const bool masked = valid < C::kBN;
+        uint32_t p0[32], p1[32];
+        // The exponential phases of the two WGs run in strict turns (named
+        // barriers kSeqBar + q): each gets the sub-partitions' MUFU / FMA
+        // pipes alone instead of both slowing down when their phases overlap.
+        if constexpr (kSeq) named_bar_sync(C::kSeqBar + q, 256);
+        float neg, rs;
+        bool redo = true;
+        if (kSpec && j > 0 && !masked) {
+          float mx;
+          neg = -m * sl2;
+          rs = exp_rowsum_pack_max<kBF16, kEmuPer16>(s, sl2, neg, p0, mx);
+          trace_stamp(args, trq, q, j, 8);
+          redo = __any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f);
+          if (redo) rescale(fmaxf(mx, m));
+        } else {
           const float mx = row_max();
           trace_stamp(args, trq, q, j, 8);
           if (__any_sync(0xffffffffu, (mx - m) * sl2 > 8.0f)) {
@@ -463,26 +592,19 @@ __global__ void __launch_bounds__(384, 1)
               rescale(m_new);
           }
         }
-        // P half h = scores [64h, 64h+64) -> packed TMEM columns [32h, 32h+32)
-        // of S_q (S is already in registers).  Padded tiles take an all-MUFU
-        // copy (exact zeros for -inf scores).  The TMEM store of half 0 is
-        // waited for only after half 1's exponentials: the ~200-clk store
-        // latency leaves the critical path; GEMM-II on half 0 then overlaps
-        // the store and publication of half 1.
-        const float neg = -m * sl2;
-        const bool masked = valid < C::kBN;
-        uint32_t p0[32], p1[32];
-        // The exponential phases of the two WGs run in strict turns (named
-        // barriers kSeqBar + q): each gets the sub-partitions' MUFU / FMA
-        // pipes alone instead of both slowing down when their phases overlap.
-        if constexpr (kSeq) named_bar_sync(C::kSeqBar + q, 256);
-        float rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
-                          : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+        prof.mark(2);
+        if (redo) {
+          neg = -m * sl2;
+          rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
+                      : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+        }
         trace_stamp(args, trq, q, j, 9);
+        prof.mark(3);
         tmem_st32x32b_x32(tS, p0);
         rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
                      : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
         if constexpr (kSeq) named_bar_arrive(C::kSeqBar + (q ^ 1), 256);
+        prof.mark(4);
         trace_stamp(args, trq, q, j, 10);
         // every thread arrives once its own TMEM stores have completed (no
         // lane-0 branch, no warp reconvergence on the critical path)
@@ -496,6 +618,7 @@ __global__ void __launch_bounds__(384, 1)
         tmem_st32x32b_x32(tS + 32, p1);
         publish(1);
         l += rs;
+        prof.mark(5);
         trace_stamp(args, trq, q, j, 3);
 #ifdef FMHA_TRACE_BUILD
         // per-warp completion times of the first unit: trace[(2*n_kv + j)*16 + warp]
@@ -515,10 +638,15 @@ __global__ void __launch_bounds__(384, 1)
       // WG's latest use has been read by its TMA store.  That use itself
       // waited for this WG's previous use, so stage_free[q^1] is at most one
       // phase away from the awaited one and the parity wait is exact.
-      if (q == 1)
-        mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
-      else if (i > 0)
-        mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
+      if constexpr (!C::kOInQ) {
+        if (q == 1)
+          mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
+        else if (i > 0)
+          mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
+      }
+      // kOInQ: Q_q's buffer is free (the unit's S GEMMs completed before the
+      // PVs that o_full observed) and is reloaded only after this store
+      uint8_t* stage = C::kOInQ ? sQ + ((i % C::kQStages) * 2 + q) * C::kQTileBytes : sO;
       const float inv = 1.0f / l;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
@@ -529,7 +657,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int t = 0; t < 16; ++t)
           h2[t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
         // columns c*32 .. c*32+31 = four 16-B units of 64-column atom c/2
-        uint8_t* rowp = sO + (c >> 1) * (C::kBM * 128) + r * 128;
+        uint8_t* rowp = stage + (c >> 1) * (C::kBM * 128) + r * 128;
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int unit = ((c & 1) * 4 + v) ^ (r & 7);  // 128-B swizzle
@@ -539,10 +667,11 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
       mbar_arrive(&o_empty[q]);  // O_q drained from TMEM (all 128 threads)
-      mbar_arrive(stage_ready);  // this thread's row staged
+      mbar_arrive(&stage_ready[C::kOInQ ? q : 0]);  // this thread's row staged
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
       if (row < args.n_q && args.lse != nullptr)
         args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
+      prof.mark(6);
       trace_stamp(args, trq, q, n_kv - 1, 7);
 #ifdef FMHA_TRACE_BUILD
       if (tr && i < 8 && r == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 3 + q] = clock64();
@@ -551,6 +680,7 @@ __global__ void __launch_bounds__(384, 1)
     // consume WG 1's last hand-over so no named barrier is left half-arrived
     if constexpr (kSeq)
       if (q == 0) named_bar_sync(C::kSeqBar, 256);
+    prof.flush(args, warp);
   }
 
   tc_fence_before();

@@ -137,6 +137,39 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
   return (a0 + b0) + (a1 + b1);
 }
 
+// exp_rowsum_pack over s[0, 64) with the full 128-column row max of s
+// folded into the same instruction stream (FMNMX3 on the ALU pipe fills the
+// MUFU / FMA latency slots): the speculative form of a tile's first half,
+// exponentiated against the previous tile's max while the new one is reduced.
+template <bool kBF16, int kEmuPer16>
+__device__ __forceinline__ float exp_rowsum_pack_max(const float (&s)[128], float c, float neg_mc,
+                                                     uint32_t (&p)[32], float& row_max) {
+  const uint64_t c2 = f2_pack(c, c);
+  const uint64_t nm2 = f2_pack(neg_mc, neg_mc);
+  uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = f2_pack(0.f, 0.f);
+  float mx[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint64_t x = ffma2(f2_pack(s[2 * i], s[2 * i + 1]), c2, nm2);
+    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    if (i & 1)
+      acc1 = fadd2(acc1, e);
+    else
+      acc0 = fadd2(acc0, e);
+    p[i] = pack2_x2<kBF16>(e);
+    // 4 more columns of the max per pair (columns 4..127 over the 32 pairs)
+    if (i < 31) {
+      const int b = 4 + 4 * i;
+      mx[i & 3] = fmaxf(mx[i & 3], fmaxf(s[b], fmaxf(s[b + 1], fmaxf(s[b + 2], s[b + 3]))));
+    }
+  }
+  row_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+  float a0, a1, b0, b1;
+  f2_unpack(acc0, a0, a1);
+  f2_unpack(acc1, b0, b1);
+  return (a0 + b0) + (a1 + b1);
+}
+
 template <uint32_t kRegs>
 __device__ __forceinline__ void reg_alloc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegs));
