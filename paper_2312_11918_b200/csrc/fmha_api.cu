@@ -200,7 +200,8 @@ fmha_status launch_split(const fmha_fwd_params* p, const CUtensorMap& mq, const 
 // SM.  `mk64` / `mv64` are K / V maps with 64-row boxes.
 template <bool BF16, int EMU>
 fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
-                       const CUtensorMap& mv64, void* o, float* lse, cudaStream_t st, int64_t nq) {
+                       const CUtensorMap& mv64, const CUtensorMap& mo, void* o, float* lse, cudaStream_t st,
+                       int64_t nq) {
   using Cfg = fmha_b200::FwdCfgD64;
   auto kern = fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>;
   if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_d64_kernel<BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
@@ -222,7 +223,7 @@ fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CU
   a.scale_log2 = a.scale * 1.4426950408889634f;
   a.trace = nullptr;
   const int grid = std::min(a.n_units, 2 * num_sms());
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk64, mv64, a);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk64, mv64, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch (d=64)");
   g_last_launches = 1;
@@ -231,7 +232,8 @@ fmha_status launch_d64(const fmha_fwd_params* p, const CUtensorMap& mq, const CU
 
 template <int D, int BN, bool BF16, int EMU>
 fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk64,
-                        const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
+                        const CUtensorMap& mv, const CUtensorMap& mo, void* o, float* lse, cudaStream_t st,
+                        int64_t nq) {
   using Cfg = fmha_b200::FwdCfgPair<D, BN>;
   auto kern = fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>;
   if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_pair_kernel<D, BN, BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
@@ -262,7 +264,7 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mk64, mv, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mk64, mv, mo, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch (CTA pair)");
   g_last_launches = 1;
@@ -271,7 +273,8 @@ fmha_status launch_pair(const fmha_fwd_params* p, const CUtensorMap& mq, const C
 
 template <int D, bool BF16, int BN>
 fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
-                      const CUtensorMap& mv, void* o, float* lse, cudaStream_t st, int64_t nq) {
+                      const CUtensorMap& mv, const CUtensorMap& mo, void* o, float* lse, cudaStream_t st,
+                      int64_t nq) {
   using Cfg = fmha_b200::FwdCfgST<D, BN>;
   auto kern = fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>;
   if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_st_kernel<D, BF16, BN>>(Cfg::kSmemAlloc); e != cudaSuccess)
@@ -291,7 +294,7 @@ fmha_status launch_st(const fmha_fwd_params* p, const CUtensorMap& mq, const CUt
   a.trace = nullptr;
   dim3 grid(static_cast<unsigned>((nq + Cfg::kBM - 1) / Cfg::kBM), static_cast<unsigned>(p->h),
             static_cast<unsigned>(p->L));
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, a);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
@@ -523,15 +526,15 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       CUtensorMap mkh, mvh;
       if (!make_map(&mkh, k, p->dtype, p, p->k_stride, 32) || !make_map(&mvh, v, p->dtype, p, p->v_stride, 64))
         return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K/V maps of the CTA-pair kernel)");
-      return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, o, lse, st, nq)
-                : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, o, lse, st, nq);
+      return bf ? launch_pair<128, 64, true, 2>(p, mq, mkh, mvh, mo, o, lse, st, nq)
+                : launch_pair<128, 64, false, 2>(p, mq, mkh, mvh, mo, o, lse, st, nq);
     }
     case Kernel::kD64TwoCta: {
       CUtensorMap mk64, mv64;
       if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
         return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
-      return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, o, lse, st, nq)
-                : launch_d64<false, 4>(p, mq, mk64, mv64, o, lse, st, nq);
+      return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, mo, o, lse, st, nq)
+                : launch_d64<false, 4>(p, mq, mk64, mv64, mo, o, lse, st, nq);
     }
     case Kernel::kPingPong64: {
       // exp2 split 6/16 (measured: +1 % over 4/16 at N = 512 / 768, equal at 256)
@@ -579,13 +582,13 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       CUtensorMap mk64;
       if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64))
         return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
-      return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, o, lse, st, nq)
-                : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, o, lse, st, nq);
+      return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, mo, o, lse, st, nq)
+                : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, mo, o, lse, st, nq);
     }
     case Kernel::kSingle256:
     default:
-      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, o, lse, st, nq)
-                : launch_st<256, false, 128>(p, mq, mk, mv, o, lse, st, nq);
+      return bf ? launch_st<256, true, 128>(p, mq, mk, mv, mo, o, lse, st, nq)
+                : launch_st<256, false, 128>(p, mq, mk, mv, mo, o, lse, st, nq);
   }
 }
 

@@ -14,14 +14,17 @@
 //        warps 0-3 softmax Q tile 0, 4-7 softmax Q tile 1 (thread = row =
 //        TMEM lane), warp 8 TMA producer, warp 9 MMA issuer.  No register
 //        reallocation (640 threads per SM leave ~100 registers per thread).
-//   smem: Q 2 x 16 KB, K/V ring 8 x 8 KB (64 rows x 128 B), barriers.
+//   smem: Q 2 x 16 KB, K/V ring 7 x 8 KB (64 rows x 128 B), one 16 KB O
+//        staging tile shared by the two WGs in turns, barriers.
 //   TMEM: S0 [0,64) S1 [64,128) O0 [128,192) O1 [192,256); P (16-bit)
 //        aliases the first 32 columns of its S tile (TS-form PV MMA).
 //   MMA order per unit: S0(0) S1(0) | PV0(j-1) S0(j) PV1(j-1) S1(j) | ... |
 //        PV0(n-1) PV1(n-1); in-order completion makes "S_q(j) done" imply
 //        "PV_q(j-1) done" (conditional O rescale without an extra barrier).
-//   Epilogue: O_q -> registers (o_empty released) -> x(1/Sigma) -> 16-bit ->
-//        direct 16-B global stores + LSE.
+//   Epilogue: O_q -> x(1/Sigma) -> 16-bit -> the swizzled staging tile (the
+//        two WGs take it in turns: WG0 unit i, WG1 unit i, WG0 unit i+1, ...)
+//        -> one TMA store issued by the WG's first thread, which releases the
+//        tile to the other WG once the store has read it; + LSE.
 #pragma once
 
 #include <cuda.h>
@@ -40,11 +43,12 @@ struct FwdCfgD64 {
   static constexpr int kBN = 64;
   static constexpr int kQTileBytes = kBM * D * 2;    // 16 KB
   static constexpr int kKVTileBytes = kBN * D * 2;   // 8 KB
-  static constexpr int kStages = 8;
+  static constexpr int kStages = 7;
   static constexpr int kSmemQ = 2 * kQTileBytes;
+  static constexpr int kSmemO = kQTileBytes;  // epilogue staging, shared by both WGs
   static constexpr int kSmemRing = kStages * kKVTileBytes;
-  static constexpr int kNumBars = 2 + 2 * kStages + 2 + 2 + 2 + 2;
-  static constexpr int kSmemBytes = kSmemQ + kSmemRing + kNumBars * 8 + 16;
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 + 2 + 2 + 2 + 2;
+  static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;
   static constexpr int kThreads = 320;
   static constexpr int kLoadWarp = 8;
@@ -59,6 +63,7 @@ __global__ void __launch_bounds__(320, 2)
     fmha_fwd_d64_kernel(const __grid_constant__ CUtensorMap tmQ,  // box 128 rows
                         const __grid_constant__ CUtensorMap tmK,  // box 64 rows
                         const __grid_constant__ CUtensorMap tmV,  // box 64 rows
+                        const __grid_constant__ CUtensorMap tmO,  // box 128 rows (epilogue TMA store)
                         const FwdArgs args) {
   using C = FwdCfgD64;
   constexpr int D = C::D;
@@ -66,7 +71,8 @@ __global__ void __launch_bounds__(320, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
-  uint8_t* sRing = smem + C::kSmemQ;
+  uint8_t* sO = smem + C::kSmemQ;
+  uint8_t* sRing = sO + C::kSmemO;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing);
   uint64_t* q_full = bars;                   // [1]
   uint64_t* q_empty = bars + 1;              // [1]
@@ -76,7 +82,8 @@ __global__ void __launch_bounds__(320, 2)
   uint64_t* p_full = s_full + 2;             // [2]
   uint64_t* o_full = p_full + 2;             // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* stage_free = o_empty + 2;        // [2]: WG q's use of the staging tile read by its store
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_free + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -94,6 +101,7 @@ __global__ void __launch_bounds__(320, 2)
       mbar_init(&p_full[q], 4);  // one arrival per softmax warp
       mbar_init(&o_full[q], 1);
       mbar_init(&o_empty[q], 4);
+      mbar_init(&stage_free[q], 1);
     }
     fence_mbar_init();
   }
@@ -291,33 +299,34 @@ __global__ void __launch_bounds__(320, 2)
         if (lane == 0) mbar_arrive(&p_full[q]);
       }
 
-      // epilogue: O_q -> registers (then O_q's TMEM is free) -> 16-bit -> global
+      // epilogue (rowwise_finalize, attention.cpp:68-73): O_q -> x(1/Sigma)
+      // -> 16-bit -> the swizzled staging tile -> TMA store.  The WGs take
+      // the tile in strict turns: before writing, wait until the OTHER WG's
+      // latest use has been read by its store (that use waited for this WG's
+      // previous one, so the parity wait is exact).
       mbar_wait(&o_full[q], static_cast<uint32_t>(i) & 1);
       tc_fence_after();
-      const float inv = 1.0f / l;
-      uint32_t h2[D / 2];
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32x32b_x32(tO + c * 32, o);
-#pragma unroll
-        for (int t = 0; t < 16; ++t)
-          h2[c * 16 + t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
-      }
+      if (q == 1)
+        mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
+      else if (i > 0)
+        mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
+      stage_o_tile<D, kBF16>(tO, sO, r, 1.0f / l);
       tc_fence_before();
+      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[q]);
-      const int row = qb * 2 * C::kBM + q * C::kBM + r;
-      if (row < args.n_q) {
-        uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
-                         static_cast<int64_t>(row) * args.o_sn + static_cast<int64_t>(head) * args.o_sh;
-#pragma unroll
-        for (int v = 0; v < D / 8; ++v)
-          st_global_v4(orow + v * 8, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2], h2[4 * v + 3]);
-        if (args.lse != nullptr)
-          args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
+      if (lane == 0) mbar_arrive(&o_empty[q]);  // O_q drained from TMEM
+      named_bar_sync(1 + q, 128);                // the WG's 128 rows staged
+      if (r == 0) {
+        tma_store_4d(&tmO, sO, 0, head, qb * 2 * C::kBM + q * C::kBM, b);
+        tma_store_commit();
+        tma_store_wait_read();
+        mbar_arrive(&stage_free[q]);
       }
+      const int row = qb * 2 * C::kBM + q * C::kBM + r;
+      if (row < args.n_q && args.lse != nullptr)
+        args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
     }
+    if (r == 0) tma_store_wait_all();
   }
 
   tc_fence_before();

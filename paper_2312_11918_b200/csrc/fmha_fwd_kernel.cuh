@@ -60,7 +60,7 @@
 namespace fmha_b200 {
 
 struct FwdArgs {
-  void* o;                   // BSHD output (direct-store epilogue of the d=256 kernel)
+  void* o;                   // BSHD output (informational: every kernel stores O by TMA through tmO)
   int64_t o_sb, o_sn, o_sh;  // output strides (elements)
   float* lse;        // [L][h][N] fp32 or nullptr
   int N, H, L;      // N: key/value length (and the LSE row stride)
@@ -169,6 +169,28 @@ constexpr bool kSpec = FMHA_SPEC != 0;  // speculative first half (see the softm
 #ifndef FMHA_KV_PREFETCH
 #define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
 #endif
+
+// Epilogue helper (rowwise_finalize, attention.cpp:68-73): this thread's row
+// of a 128-row O tile, TMEM columns [tO, tO + D) -> x inv -> 16-bit -> the
+// 128-B-swizzled TMA layout at `stage` (D/64 atoms of 128 rows x 128 B).
+template <int D, bool kBF16>
+__device__ __forceinline__ void stage_o_tile(uint32_t tO, uint8_t* stage, int r, float inv) {
+#pragma unroll
+  for (int c = 0; c < D / 32; ++c) {
+    uint32_t o[32];
+    tmem_ld32x32b_x32(tO + c * 32, o);
+    uint32_t h2[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      h2[t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+    uint8_t* rowp = stage + (c >> 1) * (128 * 128) + r * 128;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int unit = ((c & 1) * 4 + v) ^ (r & 7);  // 128-B swizzle
+      st_shared_v4(rowp + unit * 16, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2], h2[4 * v + 3]);
+    }
+  }
+}
 
 // unit -> (b, head, q-block)
 __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int& head, int& qb) {

@@ -76,7 +76,9 @@ template <int D, bool kBF16, int kBN = 128, int kEmuPer16 = 4>
 __global__ void __launch_bounds__(192, FwdCfgST<D, kBN>::kCtasPerSm)
     fmha_fwd_st_kernel(const __grid_constant__ CUtensorMap tmQ,
                        const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
+                       const __grid_constant__ CUtensorMap tmV,
+                       const __grid_constant__ CUtensorMap tmO,  // box 128 rows (epilogue TMA store)
+                       const FwdArgs args) {
   using C = FwdCfgST<D, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -293,30 +295,20 @@ __global__ void __launch_bounds__(192, FwdCfgST<D, kBN>::kCtasPerSm)
       mbar_arrive(&p_full[buf]);
     }
 
+    // epilogue: O staged in the (now free) Q tile buffer, TMA-stored
     mbar_wait(o_full, 0);
     tc_fence_after();
     const int row = qrow0 + r;
-    const bool row_ok = row < args.n_q;
-    const float inv = 1.0f / l;
-    uint16_t* orow = reinterpret_cast<uint16_t*>(args.o) + static_cast<int64_t>(b) * args.o_sb +
-                     static_cast<int64_t>(row_ok ? row : 0) * args.o_sn +
-                     static_cast<int64_t>(head) * args.o_sh;
+    stage_o_tile<D, kBF16>(tO, sQ, r, 1.0f / l);
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32x32b_x32(tO + c * 32, o);
-      uint32_t h2[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        h2[i] = pack2<kBF16>(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-      if (row_ok) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          st_global_v4(orow + c * 32 + v * 8, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2],
-                       h2[4 * v + 3]);
-      }
+      for (int c = 0; c < C::kChunks; ++c) tma_store_4d(&tmO, sQ + c * C::kBM * 128, c * 64, head, qrow0, b);
+      tma_store_commit();
+      tma_store_wait_all();
     }
-    if (row_ok && args.lse != nullptr)
+    if (row < args.n_q && args.lse != nullptr)
       args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
   }
 
