@@ -120,10 +120,6 @@ struct Prof {
 #endif
 };
 
-#ifndef FMHA_O_IN_Q
-#define FMHA_O_IN_Q 0
-#endif
-
 template <int D>
 struct FwdCfg {
   static_assert(D == 64 || D == 128, "this kernel handles head dim 64 and 128");
@@ -132,17 +128,15 @@ struct FwdCfg {
   static constexpr int kChunks = D / 64;  // 128-B swizzle atoms along d
   static constexpr int kQTileBytes = kBM * D * 2;
   static constexpr int kKVTileBytes = kBN * D * 2;
-  // FMHA_O_IN_Q=1 (d = 128, measured, not the default): O_q is staged for its
-  // TMA store in Q_q's own buffer (free once the unit's last S GEMMs are done;
-  // the next unit's Q load waits for both stores to be read), which buys a
-  // fifth 32 KB K/V slot.  The MMA warp's K/V waits did not shrink (272 vs
-  // 273 clk per period, tools/prof_phases.py) while every unit transition
-  // gained a Q-reload bubble: c3 1201 vs 1221 TFLOP/s, N=1024 -12 %.
-  static constexpr bool kOInQ = D == 128 && FMHA_O_IN_Q != 0;
-  static constexpr int kStages = D == 64 ? 8 : (kOInQ ? 5 : 4);  // K/V ring depth
+  static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
   static constexpr int kQStages = D == 64 ? 2 : 1;  // Q double-buffered when it fits
   static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
-  static constexpr int kSmemO = kOInQ ? 0 : kQTileBytes;  // epilogue staging, shared by both Q tiles
+  // O staging for the TMA store: one tile per softmax WG when it fits (d = 64),
+  // else one tile the two WGs take in turns (d = 128: 224 KB are in use).
+  // (Measured alternative at d = 128, profiles/r02_microbench.txt: staging in
+  // the finished unit's Q buffer to buy a fifth K/V slot -- slower.)
+  static constexpr int kOBufs = D == 64 ? 2 : 1;
+  static constexpr int kSmemO = kOBufs * kQTileBytes;
   static constexpr int kSmemRing = kStages * kKVTileBytes;
   static constexpr int kPChunks = 2;  // P published in two halves of 64 kv rows
   static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 8;
@@ -225,7 +219,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* o_full = p_full + 2 * C::kPChunks;  // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
   uint64_t* stage_free = o_empty + 2;        // [2]: WG q's use of the O staging tile read by its TMA store
-  uint64_t* stage_ready = stage_free + 2;    // [2] O_q staged by softmax WG q (kOInQ: one per WG)
+  uint64_t* stage_ready = stage_free + 2;    // [2] O staged (kOBufs == 2: per WG; else [0] in turns)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 2);
 
   const int warp = threadIdx.x >> 5;
@@ -243,8 +237,7 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kQStages; ++s) {
       mbar_init(&q_full[s], 1);
-      // kOInQ: the last S GEMMs' commit + the read-out of both O stores
-      mbar_init(&q_empty[s], C::kOInQ ? 3 : 1);
+      mbar_init(&q_empty[s], 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&kv_full[s], 1);
@@ -472,24 +465,22 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == C::kStoreWarp) {
       // ------------------------------------------------- O store warp --
       // Uses of the staging tile alternate WG0, WG1 per unit: use k = 2i+q.
-      // kOInQ: O_q sits in Q_q's buffer; once both stores of the unit have
-      // been read out, the Q stage is released to the producer (q_empty).
       if (lane == 0) {
         uint32_t k = 0;
         int i = 0;
         for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
           int b, head, qb;
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
-          const int qs = i % C::kQStages;
           for (int q = 0; q < 2; ++q, ++k) {
-            const uint8_t* src = C::kOInQ ? sQ + (qs * 2 + q) * C::kQTileBytes : sO;
-            mbar_wait(&stage_ready[C::kOInQ ? q : 0], C::kOInQ ? (static_cast<uint32_t>(i) & 1) : (k & 1));
+            const bool own = C::kOBufs == 2;  // per-WG tiles: use i of WG q; shared: use k = 2i + q
+            mbar_wait(&stage_ready[own ? q : 0], own ? (static_cast<uint32_t>(i) & 1) : (k & 1));
+            const uint8_t* src = sO + (own ? q : 0) * C::kQTileBytes;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
               tma_store_4d(&tmO, src + c * C::kBM * 128, c * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
             tma_store_commit();
             tma_store_wait_read();
-            mbar_arrive(C::kOInQ ? &q_empty[qs] : &stage_free[q]);
+            mbar_arrive(&stage_free[q]);
           }
         }
         tma_store_wait_all();
@@ -660,36 +651,20 @@ __global__ void __launch_bounds__(384, 1)
       // WG's latest use has been read by its TMA store.  That use itself
       // waited for this WG's previous use, so stage_free[q^1] is at most one
       // phase away from the awaited one and the parity wait is exact.
-      if constexpr (!C::kOInQ) {
+      if constexpr (C::kOBufs == 2) {  // own tile: wait for this WG's previous store
+        if (i > 0) mbar_wait(&stage_free[q], static_cast<uint32_t>(i - 1) & 1);
+      } else {
         if (q == 1)
           mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
         else if (i > 0)
           mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
       }
-      // kOInQ: Q_q's buffer is free (the unit's S GEMMs completed before the
-      // PVs that o_full observed) and is reloaded only after this store
-      uint8_t* stage = C::kOInQ ? sQ + ((i % C::kQStages) * 2 + q) * C::kQTileBytes : sO;
-      const float inv = 1.0f / l;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32x32b_x32(tO + c * 32, o);
-        uint32_t h2[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t)
-          h2[t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
-        // columns c*32 .. c*32+31 = four 16-B units of 64-column atom c/2
-        uint8_t* rowp = stage + (c >> 1) * (C::kBM * 128) + r * 128;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int unit = ((c & 1) * 4 + v) ^ (r & 7);  // 128-B swizzle
-          st_shared_v4(rowp + unit * 16, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2], h2[4 * v + 3]);
-        }
-      }
+      uint8_t* stage = sO + (C::kOBufs == 2 ? q : 0) * C::kQTileBytes;
+      stage_o_tile<D, kBF16>(tO, stage, r, 1.0f / l);
       tc_fence_before();
       fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
       mbar_arrive(&o_empty[q]);  // O_q drained from TMEM (all 128 threads)
-      mbar_arrive(&stage_ready[C::kOInQ ? q : 0]);  // this thread's row staged
+      mbar_arrive(&stage_ready[C::kOBufs == 2 ? q : 0]);  // this thread's row staged
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
       if (row < args.n_q && args.lse != nullptr)
         args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m * args.scale + logf(l);
