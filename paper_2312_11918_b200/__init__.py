@@ -77,6 +77,10 @@ def lib():
         L.fmha_kernel_for.argtypes = [P]
         L.fmha_kernel_for.restype = C.c_char_p
         L.fmha_version.restype = C.c_char_p
+        L.fmha_host_quantize.argtypes = [vp, vp, C.c_int64, C.c_int]
+        L.fmha_host_quantize.restype = None
+        L.fmha_host_dequantize.argtypes = [vp, vp, C.c_int64, C.c_int]
+        L.fmha_host_dequantize.restype = None
         L.fmha_host_f32_to_16.argtypes = [C.c_float, C.c_int]
         L.fmha_host_f32_to_16.restype = C.c_uint16
         L.fmha_host_16_to_f32.argtypes = [C.c_uint16, C.c_int]

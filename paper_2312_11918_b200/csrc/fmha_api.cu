@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -340,7 +341,8 @@ struct InChunk {
   int64_t b0, b1;
   std::vector<Chunk> groups;
 };
-std::vector<InChunk> plan_chunks(const fmha_fwd_params* p, size_t in_bytes, size_t out_bytes) {
+std::vector<InChunk> plan_chunks(const fmha_fwd_params* p, size_t in_bytes, size_t out_bytes,
+                                 bool head_groups = true) {
   std::vector<InChunk> out;
   const size_t batch_in = static_cast<size_t>(3 * p->N * p->h * p->d * 2);
   const size_t batch_out = static_cast<size_t>(p->N * p->h * p->d * 2);
@@ -348,7 +350,7 @@ std::vector<InChunk> plan_chunks(const fmha_fwd_params* p, size_t in_bytes, size
   for (int64_t b0 = 0; b0 < p->L; b0 += bpc) {
     InChunk c{b0, std::min(p->L, b0 + bpc), {}};
     int64_t groups = 1;
-    if (c.b1 - c.b0 == 1)
+    if (head_groups && c.b1 - c.b0 == 1)
       groups = std::min<int64_t>({p->h, 8, std::max<int64_t>(1, static_cast<int64_t>(batch_out / out_bytes))});
     const int64_t hpg = (p->h + groups - 1) / groups;
     for (int64_t h0 = 0; h0 < p->h; h0 += hpg) c.groups.push_back({c.b0, c.b1, h0, std::min(p->h, h0 + hpg)});
@@ -611,7 +613,8 @@ fmha_status fmha_fwd_host(const fmha_fwd_params* p, const void* q, const void* k
 
 fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q, const void* k, const void* v,
                                          void* o, float* lse, int device,
-                                         void (*prepare)(void*, int64_t, int64_t), void* ctx) {
+                                         void (*prepare)(void*, int64_t, int64_t), void* ctx,
+                                         void (*consume)(void*, const OutPiece&)) {
   fmha_status s = fmha_fwd_check(p);
   if (s != FMHA_OK) return s;
   if (!q || !k || !v || !o) return fail(FMHA_ERR_CONFIG, "null tensor pointer");
@@ -675,7 +678,11 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   // kernels of chunk c run and the D2H stream returns earlier head groups
   // (PCIe is full duplex, so the copy-in stream runs back to back and bounds
   // the call).
-  const std::vector<InChunk> plan = plan_chunks(p, static_cast<size_t>(16) << 20, static_cast<size_t>(4) << 20);
+  // with a consume hook (the float call shape), output pieces stay whole
+  // rows (contiguous to dequantise); otherwise single-batch chunks return
+  // in head groups of ~4 MB so the D2H tail stays short
+  const std::vector<InChunk> plan =
+      plan_chunks(p, static_cast<size_t>(16) << 20, static_cast<size_t>(4) << 20, consume == nullptr);
   size_t n_ev = plan.size();
   for (const InChunk& c : plan) n_ev += c.groups.size();
   // The last chunk, when it is one batch of a long sequence, is split by query
@@ -686,6 +693,8 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   const int64_t batch_out = p->N * p->h * p->d * 2;  // ~4 MB of O per slice, 2..16 slices
   const int64_t kSlices = std::min<int64_t>(16, std::max<int64_t>(2, batch_out >> 22));
   n_ev += slice_last ? 2 * kSlices : 0;
+  n_ev *= 2;  // + one "piece on the host" event per output piece (consume hook)
+  std::vector<std::pair<cudaEvent_t, OutPiece>> pieces;
   while (ws.ev_in.size() < n_ev) {
     cudaEvent_t a;
     if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess)
@@ -694,10 +703,27 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   }
   int launches = 0;
   size_t ev = 0;
+  // FMHA_HOST_PROFILE=1: host-side phase times of this call on stderr
+  static const bool host_prof = [] {
+    const char* e = std::getenv("FMHA_HOST_PROFILE");
+    return e && e[0] == '1';
+  }();
+  using Clock = std::chrono::steady_clock;
+  const auto t_begin = Clock::now();
+  double t_prepare = 0, t_wait = 0, t_consume = 0;
+  auto ms_since = [](Clock::time_point t) { return std::chrono::duration<double, std::milli>(Clock::now() - t).count(); };
+  // (Output pieces are consumed only once every input chunk is issued:
+  // consuming finished pieces between the input chunks' conversions was
+  // measured slower -- both are host-memory-bound, 10.4 vs 8.3-9.0 ms on c3.)
+  size_t consumed = 0;
   for (size_t ci = 0; ci < plan.size(); ++ci) {
     const InChunk& ic = plan[ci];
     const Chunk all{ic.b0, ic.b1, 0, p->h};
-    if (prepare) prepare(ctx, ic.b0, ic.b1);
+    if (prepare) {
+      const auto t0 = Clock::now();
+      prepare(ctx, ic.b0, ic.b1);
+      t_prepare += ms_since(t0);
+    }
     if (slice_last && ci + 1 == plan.size()) {
       const int64_t b = ic.b0;
       if ((e = copy_slice(dk, static_cast<const char*>(k), p->k_stride, p, all, cudaMemcpyHostToDevice, ws.s_in)) != cudaSuccess ||
@@ -732,6 +758,11 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
                                      static_cast<size_t>(n1 - n0) * 4, static_cast<size_t>(p->h),
                                      cudaMemcpyDeviceToHost, ws.s_out)) != cudaSuccess)
             return cuda_fail(e, "cudaMemcpyAsync D2H lse");
+        }
+        if (consume) {
+          cudaEvent_t landed = ws.ev_in[ev++];
+          if ((e = cudaEventRecord(landed, ws.s_out)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+          pieces.push_back({landed, OutPiece{b, b + 1, 0, p->h, n0, n1}});
         }
       }
       continue;
@@ -769,10 +800,31 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
             return cuda_fail(e, "cudaMemcpyAsync D2H lse");
         }
       }
+      if (consume) {
+        cudaEvent_t landed = ws.ev_in[ev++];
+        if ((e = cudaEventRecord(landed, ws.s_out)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        pieces.push_back({landed, OutPiece{c.b0, c.b1, c.h0, c.h1, 0, p->N}});
+      }
     }
   }
   g_last_launches = launches;
+  // hand each output piece to the caller as soon as it is on the host, while
+  // the later pieces are still being computed / copied
+  const double t_issued = ms_since(t_begin);
+  for (; consumed < pieces.size(); ++consumed) {
+    auto t0 = Clock::now();
+    if ((e = cudaEventSynchronize(pieces[consumed].first)) != cudaSuccess) return cuda_fail(e, "kernel execution");
+    t_wait += ms_since(t0);
+    t0 = Clock::now();
+    consume(ctx, pieces[consumed].second);
+    t_consume += ms_since(t0);
+  }
   if ((e = cudaStreamSynchronize(ws.s_out)) != cudaSuccess) return cuda_fail(e, "kernel execution");
+  if (host_prof)
+    std::fprintf(stderr,
+                 "fmha host pipeline: %zu input chunks, %zu output pieces | prepare %.2f ms, all issued at %.2f ms, "
+                 "waiting for pieces %.2f ms, consume %.2f ms, total %.2f ms\n",
+                 plan.size(), pieces.size(), t_prepare, t_issued, t_wait, t_consume, ms_since(t_begin));
   guard.ok = true;
   return FMHA_OK;
 }

@@ -6,7 +6,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -15,6 +17,7 @@
 #if defined(__x86_64__)
 #include <immintrin.h>
 #endif
+
 
 #include "../../include/fmha/fmha.h"
 #include "../../include/fmha/fmha.hpp"
@@ -84,22 +87,87 @@ inline float bf16_to_f32(uint16_t b) {
   return f;
 }
 
+// Persistent worker pool for the host conversions (the float call shape
+// converts ~0.5 GB per call in ~20 pieces: spawning threads per piece cost
+// more than the pieces).  One parallel region at a time (callers hold the
+// staging lock or run outside it on their own data); the calling thread
+// takes part.
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool p;
+    return p;
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // fn(t) for t in [0, T), T <= size(); returns when all are done
+  void run(int T, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> region(region_mu_);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      tasks_ = T;
+      next_ = 1;
+      pending_ = T - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  Pool() {
+    const int n = std::max(1u, std::thread::hardware_concurrency()) - 1;
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> g(mu_);
+      cv_.wait(g, [&] { return stop_ || (gen_ != seen && next_ < tasks_); });
+      if (stop_) return;
+      const int t = next_++;
+      if (next_ >= tasks_) seen = gen_;
+      const std::function<void(int)>* fn = fn_;
+      g.unlock();
+      (*fn)(t);
+      g.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, region_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int tasks_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 template <class F>
 void parallel_for(int64_t n, F&& fn) {
-  const int64_t kGrain = 1 << 20;
-  int T = static_cast<int>(std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()),
-                                             (n + kGrain - 1) / kGrain));
+  const int64_t kGrain = 1 << 18;
+  Pool& pool = Pool::get();
+  const int T = static_cast<int>(std::min<int64_t>(pool.size(), (n + kGrain - 1) / kGrain));
   if (T <= 1) {
     fn(0, n);
     return;
   }
-  std::vector<std::thread> th;
   const int64_t per = (n + T - 1) / T;
-  for (int t = 0; t < T; ++t) {
+  pool.run(T, [&](int t) {
     const int64_t a = t * per, b = std::min(n, a + per);
-    if (a < b) th.emplace_back([&, a, b] { fn(a, b); });
-  }
-  for (auto& x : th) x.join();
+    if (a < b) fn(a, b);
+  });
 }
 
 #if defined(__x86_64__)
@@ -147,26 +215,30 @@ void to_16(const float* src, uint16_t* dst, int64_t n, fmha_dtype dt) {
   });
 }
 
-void from_16(const uint16_t* src, float* dst, int64_t n, fmha_dtype dt) {
-  parallel_for(n, [&](int64_t a, int64_t b) {
-    if (dt == FMHA_BF16) {
-      for (int64_t i = a; i < b; ++i) dst[i] = bf16_to_f32(src[i]);
-      return;
-    }
+// src[a, b) -> dst[a, b), on the calling thread
+void from_16_range(const uint16_t* src, float* dst, int64_t a, int64_t b, fmha_dtype dt) {
+  if (dt == FMHA_BF16) {
+    for (int64_t i = a; i < b; ++i) dst[i] = bf16_to_f32(src[i]);
+    return;
+  }
 #if defined(__x86_64__)
-    if (has_f16c()) return from_f16_f16c(src, dst, a, b);
+  if (has_f16c()) return from_f16_f16c(src, dst, a, b);
 #endif
-    for (int64_t i = a; i < b; ++i) dst[i] = f16_to_f32(src[i]);
-  });
+  for (int64_t i = a; i < b; ++i) dst[i] = f16_to_f32(src[i]);
 }
 
-// Pinned 16-bit staging for fmha_forward_f32 (Q, K, V, O), kept across calls:
-// page-locked buffers let fmha_fwd_host's copies run at the full PCIe rate and
-// overlap its kernels; pageable vectors would be staged by the driver.
+void from_16(const uint16_t* src, float* dst, int64_t n, fmha_dtype dt) {
+  parallel_for(n, [&](int64_t a, int64_t b) { from_16_range(src, dst, a, b, dt); });
+}
+
+// Pinned staging for fmha_forward_f32 (16-bit Q, K, V, O and fp32 LSE), kept
+// across calls: page-locked buffers let fmha_fwd_host's copies run at the full
+// PCIe rate and overlap its kernels (a D2H copy into pageable memory would
+// also block the calling thread until the copy is done).
 struct Staging {
   std::mutex mu;
   uint16_t* buf = nullptr;
-  size_t elems = 0;
+  size_t bytes = 0;
 };
 Staging& staging() {
   static Staging s;
@@ -207,47 +279,77 @@ fmha_status fmha_forward_f32(const float* q, const float* k, const float* v, int
     return FMHA_ERR_CONFIG;
   }
   const int64_t n = L * N * h * d;
+  const int64_t n_lse = L * h * N;
+  const size_t need = static_cast<size_t>(4 * n) * 2 + static_cast<size_t>(n_lse) * 4;
   Staging& stg = staging();
   std::lock_guard<std::mutex> lock(stg.mu);
-  std::vector<uint16_t> pageable;  // fallback when page-locked memory is unavailable
-  uint16_t* base = nullptr;
-  if (stg.elems >= static_cast<size_t>(4 * n)) {
-    base = stg.buf;
+  std::vector<uint8_t> pageable;  // fallback when page-locked memory is unavailable
+  uint8_t* base = nullptr;
+  if (stg.bytes >= need) {
+    base = reinterpret_cast<uint8_t*>(stg.buf);
   } else {
     if (stg.buf) cudaFreeHost(stg.buf);
     stg.buf = nullptr;
-    stg.elems = 0;
+    stg.bytes = 0;
     void* b = nullptr;
-    if (cudaHostAlloc(&b, static_cast<size_t>(4 * n) * 2, cudaHostAllocPortable) == cudaSuccess) {
+    if (cudaHostAlloc(&b, need, cudaHostAllocPortable) == cudaSuccess) {
       stg.buf = static_cast<uint16_t*>(b);
-      stg.elems = static_cast<size_t>(4 * n);
-      base = stg.buf;
+      stg.bytes = need;
+      base = static_cast<uint8_t*>(b);
     } else {
       cudaGetLastError();  // clear the allocation error, use pageable memory
-      pageable.resize(static_cast<size_t>(4 * n));
+      pageable.resize(need);
       base = pageable.data();
     }
   }
-  uint16_t *hq = base, *hk = base + n, *hv = base + 2 * n, *ho = base + 3 * n;
-  // quantise each input chunk just before the pipeline copies it, so the
-  // conversion of chunk c+1 overlaps the copies / kernels of chunk c
+  uint16_t* hq = reinterpret_cast<uint16_t*>(base);
+  uint16_t *hk = hq + n, *hv = hq + 2 * n, *ho = hq + 3 * n;
+  float* hl = lse ? reinterpret_cast<float*>(hq + 4 * n) : nullptr;
+  // Quantise each input chunk just before the pipeline copies it (the
+  // conversion of chunk c+1 overlaps the copies / kernels of chunk c), and
+  // dequantise each piece of O as soon as it is back on the host (while later
+  // pieces are still computed / copied).
   struct Ctx {
     const float *q, *k, *v;
-    uint16_t *hq, *hk, *hv;
-    int64_t per_batch;
+    uint16_t *hq, *hk, *hv, *ho;
+    const float* hl;
+    float *o, *lse;
+    int64_t N, h, d;
     fmha_dtype dt;
-  } ctx{q, k, v, hq, hk, hv, N * h * d, dtype};
+  } ctx{q, k, v, hq, hk, hv, ho, hl, o, lse, N, h, d, dtype};
   auto prepare = [](void* c, int64_t b0, int64_t b1) {
     const Ctx& x = *static_cast<const Ctx*>(c);
-    const int64_t off = b0 * x.per_batch, cnt = (b1 - b0) * x.per_batch;
+    const int64_t per_batch = x.N * x.h * x.d;
+    const int64_t off = b0 * per_batch, cnt = (b1 - b0) * per_batch;
     to_16(x.q + off, x.hq + off, cnt, x.dt);
     to_16(x.k + off, x.hk + off, cnt, x.dt);
     to_16(x.v + off, x.hv + off, cnt, x.dt);
   };
-  s = fmha_b200::fwd_host_pipeline(&p, hq, hk, hv, ho, lse, device, prepare, &ctx);
-  if (s != FMHA_OK) return s;
-  from_16(ho, o, n, dtype);
-  return FMHA_OK;
+  auto consume = [](void* c, const fmha_b200::OutPiece& pc) {
+    const Ctx& x = *static_cast<const Ctx*>(c);
+    const int64_t row = x.h * x.d;  // elements per query row (all heads)
+    for (int64_t b = pc.b0; b < pc.b1; ++b) {
+      if (pc.h0 == 0 && pc.h1 == x.h) {  // whole rows: one contiguous range
+        const int64_t off = (b * x.N + pc.n0) * row;
+        from_16(x.ho + off, x.o + off, (pc.n1 - pc.n0) * row, x.dt);
+      } else {  // a head group: (h1 - h0) * d contiguous elements per row
+        const int64_t w = (pc.h1 - pc.h0) * x.d;
+        parallel_for((pc.n1 - pc.n0) * w, [&](int64_t a, int64_t e) {
+          for (int64_t r = a / w; r * w < e; ++r) {
+            const int64_t lo = std::max(a, r * w) - r * w, hi = std::min(e, (r + 1) * w) - r * w;
+            const int64_t off = (b * x.N + pc.n0 + r) * row + pc.h0 * x.d;
+            from_16_range(x.ho + off, x.o + off, lo, hi, x.dt);
+          }
+        });
+      }
+      if (x.lse)
+        for (int64_t hh = pc.h0; hh < pc.h1; ++hh) {
+          const int64_t off = (b * x.h + hh) * x.N + pc.n0;
+          std::memcpy(x.lse + off, x.hl + off, static_cast<size_t>(pc.n1 - pc.n0) * 4);
+        }
+    }
+  };
+  return fmha_b200::fwd_host_pipeline(&p, hq, hk, hv, ho, hl, device, prepare, &ctx, consume);
 }
 
 }  // extern "C"
