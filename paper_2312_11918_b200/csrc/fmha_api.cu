@@ -57,8 +57,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 4-D map over a BSHD tensor: dims (d, h, N, L), box (64, 1, rows, 1), 128-B
 // swizzle -- each box lands in shared memory as `rows` x 128 B swizzle atoms,
 // exactly the K-major SW128 canonical layout tcgen05 descriptors expect.
+// Descriptor cache (per host thread, no locking): small calls re-use the
+// same tensors every step, and encoding 4-6 maps per call is a fixed host
+// cost of several microseconds.  Keyed by every input of the encoding.
+struct MapKey {
+  const void* ptr;
+  int64_t d, h, N, L, s0, s1, s2;
+  int box_rows, dt;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && d == o.d && h == o.h && N == o.N && L == o.L && s0 == o.s0 && s1 == o.s1 &&
+           s2 == o.s2 && box_rows == o.box_rows && dt == o.dt;
+  }
+};
+struct MapCache {
+  static constexpr int kSize = 32;
+  MapKey key[kSize];
+  CUtensorMap map[kSize];
+  bool used[kSize] = {};
+  int next = 0;
+};
+
 bool make_map(CUtensorMap* map, const void* ptr, fmha_dtype dt, const fmha_fwd_params* p,
               const int64_t stride[3], int box_rows) {
+  thread_local MapCache cache;
+  const MapKey k{ptr, p->d, p->h, p->N, p->L, stride[0], stride[1], stride[2], box_rows, static_cast<int>(dt)};
+  for (int i = 0; i < MapCache::kSize; ++i)
+    if (cache.used[i] && cache.key[i] == k) {
+      *map = cache.map[i];
+      return true;
+    }
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(p->d), static_cast<cuuint64_t>(p->h),
@@ -72,7 +99,13 @@ bool make_map(CUtensorMap* map, const void* ptr, fmha_dtype dt, const fmha_fwd_p
                   4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  const int slot = cache.next;
+  cache.next = (cache.next + 1) % MapCache::kSize;
+  cache.key[slot] = k;
+  cache.map[slot] = *map;
+  cache.used[slot] = true;
+  return true;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
