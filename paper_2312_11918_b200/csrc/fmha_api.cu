@@ -428,6 +428,7 @@ struct Tuning {
   bool pair_ok, d64_ok;
   int emu64, emu128;
   int split;  // split-row ping-pong for d <= 128 (FMHA_TUNE_SPLIT)
+  int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -436,7 +437,7 @@ const Tuning& tuning() {
       return e ? std::atoi(e) : dflt;
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
-                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0)};
+                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192)};
   }();
   return t;
 }
@@ -459,7 +460,7 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kPair128, kPair256, k
 Kernel select_kernel(const fmha_fwd_params* p) {
   const Tuning& t = tuning();
   if (p->d == 64) return t.d64_ok && p->N >= 1024 ? Kernel::kD64TwoCta : Kernel::kPingPong64;
-  if (p->d == 128) return t.pair_ok && p->N >= 8192 ? Kernel::kPair128 : Kernel::kPingPong128;
+  if (p->d == 128) return t.pair_ok && p->N >= t.pair128_min_n ? Kernel::kPair128 : Kernel::kPingPong128;
   return t.pair_ok && p->N > 128 ? Kernel::kPair256 : Kernel::kSingle256;
 }
 

@@ -1,7 +1,7 @@
-"""Copy one GPU run's outputs (tools/exp/final.sh -> gpurun_out/) into profiles/<tag>_*
+"""Copy one GPU run's outputs (tools/exp/final_r2.sh -> gpurun_out/) into profiles/<tag>_*
 and refresh profiles/ncu_summary.json (the bench's roofline.traffic source).
 
-    python tools/refresh_profiles.py r01f
+    python tools/refresh_profiles.py r02a
 """
 import csv
 import io
@@ -23,7 +23,8 @@ WANT = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__by
         "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
-        "launch__block_size"]
+        "launch__block_size", "lts__t_sectors_op_write.sum", "lts__t_requests_op_write.sum",
+        "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -34,14 +35,16 @@ def ncu_metrics(rep):
 
 
 def main(tag):
-    for c in ("c1", "c2", "c3", "c4", "c5"):
-        shutil.copy(os.path.join(OUT, f"bench_{c}.json"), os.path.join(PROF, f"{tag}_bench_{c}.json"))
-    shutil.copy(os.path.join(OUT, "bench_ref.json"), os.path.join(PROF, f"{tag}_bench_reference.json"))
-    shutil.copy(os.path.join(OUT, "launches_c3.csv"), os.path.join(PROF, f"{tag}_c3_launches.csv"))
-    shutil.copy(os.path.join(OUT, "sweep.txt"), os.path.join(PROF, f"{tag}_table1_sweep.txt"))
+    for src, dst in (("bench_default.json", "bench_default.json"), ("bench_ref.json", "bench_reference.json"),
+                     ("launches_c3.csv", "c3_launches.csv"), ("sweep.txt", "table1_sweep.txt"),
+                     ("sustained.txt", "sustained.txt"), ("phases_c3.txt", "phases_c3.txt"),
+                     ("phases_c2.txt", "phases_c2.txt"), ("gpu_tests_all.txt", "gpu_tests.txt"),
+                     ("smoke.txt", "smoke.txt")):
+        if os.path.exists(os.path.join(OUT, src)):
+            shutil.copy(os.path.join(OUT, src), os.path.join(PROF, f"{tag}_{dst}"))
     summary_path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
-    for c in ("c3", "c4", "c5"):
+    for c in ("c2", "c3", "c4", "c5"):
         rep = os.path.join(OUT, f"prof_{c}.ncu-rep")
         if not os.path.exists(rep):
             continue
