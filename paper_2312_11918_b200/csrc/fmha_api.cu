@@ -25,6 +25,7 @@
 #include "fmha_fwd_st_kernel.cuh"
 #include "fmha_fwd_kernel.cuh"
 #include "fmha_fwd_split_kernel.cuh"
+#include "fmha_fwd_dbs_kernel.cuh"
 
 namespace {
 
@@ -193,6 +194,35 @@ fmha_status launch_d128(const fmha_fwd_params* p, const CUtensorMap& mq, const C
   kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  g_last_launches = 1;
+  return FMHA_OK;
+}
+
+// The double-buffered-S d=128 kernel: one 128-row Q tile per unit, one
+// persistent CTA per SM.
+template <bool BF16, int EMU>
+fmha_status launch_dbs(const fmha_fwd_params* p, const CUtensorMap& mq, const CUtensorMap& mk,
+                       const CUtensorMap& mv, const CUtensorMap& mo, float* lse, cudaStream_t st, int64_t nq) {
+  using Cfg = fmha_b200::FwdCfgDbs;
+  auto kern = fmha_b200::fmha_fwd_dbs_kernel<BF16, EMU>;
+  if (cudaError_t e = ensure_smem_attr<fmha_b200::fmha_fwd_dbs_kernel<BF16, EMU>>(Cfg::kSmemAlloc); e != cudaSuccess)
+    return cuda_fail(e, "cudaFuncSetAttribute");
+  fmha_b200::FwdArgs a{};
+  a.lse = lse;
+  a.N = static_cast<int>(p->N);
+  a.n_q = static_cast<int>(nq);
+  a.H = static_cast<int>(p->h);
+  a.L = static_cast<int>(p->L);
+  a.n_kv_tiles = static_cast<int>((p->N + Cfg::kBN - 1) / Cfg::kBN);
+  a.n_qblocks = static_cast<int>((nq + Cfg::kBM - 1) / Cfg::kBM);
+  a.n_units = a.n_qblocks * a.H * a.L;
+  a.scale = resolve_scale(p);
+  a.scale_log2 = a.scale * 1.4426950408889634f;
+  a.trace = trace_buffer(fmha_b200::kTraceSteps * 48);
+  const int grid = std::min(a.n_units, num_sms());
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemAlloc, st>>>(mq, mk, mv, mo, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch (double-buffered S)");
   g_last_launches = 1;
   return FMHA_OK;
 }
@@ -429,6 +459,7 @@ struct Tuning {
   int emu64, emu128;
   int split;  // split-row ping-pong for d <= 128 (FMHA_TUNE_SPLIT)
   int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N)
+  int dbs;                // d = 128 below pair128_min_n: double-buffered-S kernel (FMHA_TUNE_DBS)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -437,12 +468,13 @@ const Tuning& tuning() {
       return e ? std::atoi(e) : dflt;
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
-                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192)};
+                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
+                  env("FMHA_TUNE_DBS", 0)};
   }();
   return t;
 }
 
-enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kPair128, kPair256, kSingle256 };
+enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kPair256, kSingle256 };
 
 // Which kernel runs a (valid) problem; thresholds are measured crossovers
 // (profiles/r01_microbench.txt):
@@ -460,7 +492,8 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kPair128, kPair256, k
 Kernel select_kernel(const fmha_fwd_params* p) {
   const Tuning& t = tuning();
   if (p->d == 64) return t.d64_ok && p->N >= 1024 ? Kernel::kD64TwoCta : Kernel::kPingPong64;
-  if (p->d == 128) return t.pair_ok && p->N >= t.pair128_min_n ? Kernel::kPair128 : Kernel::kPingPong128;
+  if (p->d == 128)
+    return t.pair_ok && p->N >= t.pair128_min_n ? Kernel::kPair128 : t.dbs ? Kernel::kDbs128 : Kernel::kPingPong128;
   return t.pair_ok && p->N > 128 ? Kernel::kPair256 : Kernel::kSingle256;
 }
 
@@ -469,6 +502,7 @@ const char* kernel_name(Kernel k) {
     case Kernel::kPingPong64: return "fmha_fwd_sm100_kernel<64> (persistent two-Q-tile ping-pong)";
     case Kernel::kD64TwoCta: return "fmha_fwd_d64_kernel (ping-pong, 64-row K/V steps, two CTAs per SM)";
     case Kernel::kPingPong128: return "fmha_fwd_sm100_kernel<128> (persistent two-Q-tile ping-pong)";
+    case Kernel::kDbs128: return "fmha_fwd_dbs_kernel<128> (persistent, double-buffered S, eight softmax warps)";
     case Kernel::kPair128: return "fmha_fwd_pair_kernel<128,64> (CTA pairs, two CTAs per SM)";
     case Kernel::kPair256: return "fmha_fwd_pair_kernel<256,128> (CTA pairs)";
     case Kernel::kSingle256: return "fmha_fwd_st_kernel<256,128> (single CTA)";
@@ -613,6 +647,14 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
                   : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st, nq);
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
+    }
+    case Kernel::kDbs128: {
+      const int emu = tuning().emu128;
+      if (emu == 6)
+        return bf ? launch_dbs<true, 6>(p, mq, mk, mv, mo, lse, st, nq) : launch_dbs<false, 6>(p, mq, mk, mv, mo, lse, st, nq);
+      if (emu == 8)
+        return bf ? launch_dbs<true, 8>(p, mq, mk, mv, mo, lse, st, nq) : launch_dbs<false, 8>(p, mq, mk, mv, mo, lse, st, nq);
+      return bf ? launch_dbs<true, 4>(p, mq, mk, mv, mo, lse, st, nq) : launch_dbs<false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }
     case Kernel::kPair256: {
       CUtensorMap mk64;

@@ -160,6 +160,14 @@ constexpr bool kSeq = FMHA_SEQ != 0;
 #define FMHA_SPEC 0
 #endif
 constexpr bool kSpec = FMHA_SPEC != 0;  // speculative first half (see the softmax loop)
+#ifndef FMHA_PP_SOFTMAX_SLEEP_NS
+#define FMHA_PP_SOFTMAX_SLEEP_NS 0  // softmax wait for S: nanosleep between polls (0: try_wait loop)
+#endif
+constexpr uint32_t kSoftmaxWaitNs = FMHA_PP_SOFTMAX_SLEEP_NS;
+#ifndef FMHA_PP_STORE_SLEEP_NS
+#define FMHA_PP_STORE_SLEEP_NS 0  // O store warp: nanosleep between polls (measured -0.5 % at 256 ns)
+#endif
+constexpr uint32_t kStoreWaitNs = FMHA_PP_STORE_SLEEP_NS;
 #ifndef FMHA_KV_PREFETCH
 #define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
 #endif
@@ -473,7 +481,13 @@ __global__ void __launch_bounds__(384, 1)
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
           for (int q = 0; q < 2; ++q, ++k) {
             const bool own = C::kOBufs == 2;  // per-WG tiles: use i of WG q; shared: use k = 2i + q
-            mbar_wait(&stage_ready[own ? q : 0], own ? (static_cast<uint32_t>(i) & 1) : (k & 1));
+            // optional sleep between polls (measured: the spin does not cost the
+            // softmax warps of this sub-partition anything, profiles/r02_microbench.txt)
+            if constexpr (kStoreWaitNs > 0)
+              mbar_wait_backoff(&stage_ready[own ? q : 0], own ? (static_cast<uint32_t>(i) & 1) : (k & 1),
+                                kStoreWaitNs);
+            else
+              mbar_wait(&stage_ready[own ? q : 0], own ? (static_cast<uint32_t>(i) & 1) : (k & 1));
             const uint8_t* src = sO + (own ? q : 0) * C::kQTileBytes;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
@@ -518,7 +532,10 @@ __global__ void __launch_bounds__(384, 1)
         while (!mbar_test_wait(a_s_full, it & 1)) {
         }
 #else
-        mbar_wait_addr(a_s_full, it & 1);
+        if constexpr (kSoftmaxWaitNs > 0)
+          mbar_wait_backoff_addr(a_s_full, it & 1, kSoftmaxWaitNs);  // sleep: leave issue slots to the other WG
+        else
+          mbar_wait_addr(a_s_full, it & 1);
 #endif
         prof.mark(0);
         trace_stamp(args, trq, q, j, 0);

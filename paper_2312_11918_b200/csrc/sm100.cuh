@@ -110,6 +110,42 @@ __device__ __forceinline__ void mbar_arrive_addr(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
 }
 
+// Backoff variant for waiters OFF the critical path (epilogue, O store, TMA
+// producer): between polls the warp sleeps `ns` nanoseconds.  The plain
+// try_wait loop above wakes on every mbarrier event of the CTA (~40 clk per
+// iteration in practice, measured with ncu in profiles/r02_microbench.txt),
+// so an idle role warp otherwise spins and takes issue slots from the
+// softmax warps of its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_backoff_addr(uint32_t a, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+#ifdef FMHA_WATCHDOG
+  const uint64_t t0 = globaltimer_ns();
+#endif
+  while (!ok) {
+    __nanosleep(ns);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+#ifdef FMHA_WATCHDOG
+    if (!ok && globaltimer_ns() - t0 > 4000000000ull) __trap();
+#endif
+  }
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  mbar_wait_backoff_addr(smem_u32(bar), parity, ns);
+}
+
 // Spin variant for a warp with nothing else to do that sits on the critical
 // path (the MMA issuer): non-blocking test_wait, no hardware suspend.
 __device__ __forceinline__ uint32_t mbar_test_wait(uint32_t addr, uint32_t parity) {
@@ -335,6 +371,39 @@ __device__ __forceinline__ void mma_ts_k4(uint32_t d_tmem, uint32_t a_tmem, uint
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc_first)
+      : "memory");
+}
+
+// Single-thread forms of the batched issues (the calling thread issues; used
+// when one elected thread runs the whole MMA loop, no per-MMA elect.sync).
+__device__ __forceinline__ void mma_ss_k4_1t(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc_first)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_k4_1t(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred p, t;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.s32 a1, %1, 8;\n\tadd.s32 a2, %1, 16;\n\tadd.s32 a3, %1, 24;\n\t"
+      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc_first)
       : "memory");
 }

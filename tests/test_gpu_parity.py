@@ -271,3 +271,57 @@ def test_pair_kernel_matches_single_cta_kernel_bitwise(oracle, tmp_path):
     ref = np.load(tmp_path / "out.npz")
     np.testing.assert_array_equal(o.float().cpu().numpy(), ref["o"])
     np.testing.assert_array_equal(lse.cpu().numpy(), ref["lse"])
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_double_buffered_s_kernel_against_oracle(oracle, tmp_path, dt):
+    """The opt-in d = 128 double-buffered-S kernel (FMHA_TUNE_DBS=1, read once
+    per process, so it runs in a subprocess) against the oracle: ragged N
+    (masked last K/V step, TMA-clipped Q rows), several units per CTA (the
+    flat step sequence crosses unit boundaries with an odd step count), and
+    keys growing along the sequence, which force conditional O rescales in
+    the speculative half."""
+    import os
+    import subprocess
+    import sys
+    # (bf16 takes a milder key ramp: with 3x, P's 8-bit mantissa alone puts both
+    # d = 128 kernels at ~1.2e-2, tools/exp/dbs_bf16.py)
+    ramp_top = 3.0 if dt == "f16" else 2.0
+    cases = [(1, 77, 2, 1.0), (2, 1000, 3, 1.0), (1, 640, 2, ramp_top), (2, 384, 150, 1.0)]
+    probs = {}
+    for n, (L, N, h, s) in enumerate(cases):
+        q, k, v = oracle.problem(L, N, h, 128, 50 + n, dtype=dt)
+        if s != 1.0:  # keys growing along the sequence: row maxima keep rising -> O rescales
+            ramp = (1.0 + (s - 1.0) * np.arange(N, dtype=np.float32) / N)[None, :, None, None]
+            k = oracle.quantize((k * ramp).astype(np.float32), dt)
+        probs[n] = (q, k, v)
+        np.savez(tmp_path / f"in{n}.npz", q=q, k=k, v=v)
+    code = (
+        "import numpy as np, torch, paper_2312_11918_b200 as fm\n"
+        f"td = torch.bfloat16 if {dt!r} == 'bf16' else torch.float16\n"
+        f"for n in range({len(cases)}):\n"
+        f"    z = np.load({str(tmp_path)!r} + f'/in{{n}}.npz')\n"
+        "    q, k, v = (torch.from_numpy(z[x]).cuda().to(td) for x in ('q', 'k', 'v'))\n"
+        "    L, N, h, d = q.shape[0], q.shape[1], q.shape[2], q.shape[3]\n"
+        "    assert 'double-buffered' in fm.kernel_for(L, N, h, d, fm.BF16 if td == torch.bfloat16 else fm.F16)\n"
+        "    o, lse = fm.fmha_fwd(q, k, v)\n"
+        f"    np.savez({str(tmp_path)!r} + f'/out{{n}}.npz', o=o.float().cpu().numpy(), lse=lse.cpu().numpy())\n")
+    env = dict(os.environ, FMHA_TUNE_DBS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=600)
+    for n, (L, N, h, s) in enumerate(cases):
+        q, k, v = probs[n]
+        out = np.load(tmp_path / f"out{n}.npz")
+        if N * h * L > 400 * 128:  # large case: a sample of Q tiles through the tile oracle
+            tiles = [(b, hh, t) for b in range(L) for hh in (0, h // 2, h - 1) for t in (0, (N - 1) // 128)]
+            o_ref, lse_ref = oracle.fmha_tiles(q, k, v, tiles, 128, 128)
+            for ti, (b, hh, t) in enumerate(tiles):
+                r0, r1 = t * 128, min(N, t * 128 + 128)
+                res = errors(out["o"][b, r0:r1, hh], out["lse"][b, hh, r0:r1], o_ref[ti][: r1 - r0],
+                             lse_ref[ti][: r1 - r0])
+                assert_within(res, f"dbs {dt} L={L} N={N} h={h} tile {(b, hh, t)}")
+        else:
+            bm = 128 if N % 128 == 0 else N
+            o_ref, lse_ref = oracle.fmha_forward(q, k, v, bm, bm)
+            res = errors(out["o"], out["lse"], o_ref, lse_ref)
+            assert_within(res, f"dbs {dt} L={L} N={N} h={h} scale {s}")

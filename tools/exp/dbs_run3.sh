@@ -1,0 +1,4 @@
+export FMHA_TUNE_DBS=1
+FMHA_B200_LIB=build/libfmha_b200_watchdog.so timeout 120 python tools/exp/dbs_check.py 2>&1 | grep -c OK
+timeout 120 python tools/trace_dbs.py 4096 4 16 2>&1 | tail -26
+timeout 200 python tools/exp/ab.py dbs 2,6,7,10,11 2>&1 | tail -5
