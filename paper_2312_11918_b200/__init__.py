@@ -126,6 +126,41 @@ def dense_params(L, N, h, d, dtype=F16, scale=0.0) -> FwdParams:
     return p
 
 
+class _OutputPool:
+    """Recycled float32 output buffers for :func:`fmha_forward`.
+
+    A fresh 134 MB O array (config 3) costs ~4 ms of first-touch page faults
+    inside the call's dequantisation -- a third of the whole reference-shape
+    call (tools/exp/f32_path.py).  Buffers are plain bytearrays kept here; one
+    is handed out again only when no array or view refers to it any more (its
+    reference count is back to the pool's own), so a caller never sees two
+    live results share memory."""
+
+    def __init__(self, max_bytes=8 << 30):
+        self.bufs: list[bytearray] = []
+        self.max_bytes = max_bytes
+
+    def get(self, shape):
+        import sys
+        nbytes = int(np.prod(shape)) * 4
+        buf = None
+        for b in self.bufs:
+            # references: self.bufs, the loop variable, getrefcount's argument
+            if len(b) == nbytes and sys.getrefcount(b) <= 3:
+                buf = b
+                break
+        if buf is None:
+            if sum(len(b) for b in self.bufs) + nbytes > self.max_bytes:
+                self.bufs = [b for b in self.bufs if sys.getrefcount(b) > 3]
+            buf = bytearray(nbytes)
+            if nbytes >= (1 << 20):
+                self.bufs.append(buf)
+        return np.frombuffer(buf, dtype=np.float32).reshape(shape)
+
+
+_out_pool = _OutputPool()
+
+
 def fmha_forward(q, k, v, bM=64, bN=64, precision="f16emu", scale=None, return_lse=False, device=0):
     """Reference call shape (bindings.cpp:81-91) on the GPU.
 
@@ -140,8 +175,8 @@ def fmha_forward(q, k, v, bM=64, bN=64, precision="f16emu", scale=None, return_l
     if not (arrs[0].shape == arrs[1].shape == arrs[2].shape):
         raise ValueError("AttentionProblem: Q/K/V shape mismatch")
     L, N, h, d = arrs[0].shape
-    o = np.empty((L, N, h, d), np.float32)
-    lse = np.empty((L, h, N), np.float32) if return_lse else None
+    o = _out_pool.get((L, N, h, d))
+    lse = _out_pool.get((L, h, N)) if return_lse else None
     st = lib().fmha_forward_f32(arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
                                 L, N, h, d, bM, bN, dt, float(scale or 0.0), o.ctypes.data,
                                 lse.ctypes.data if lse is not None else None, device)
