@@ -120,6 +120,10 @@ struct Prof {
 #endif
 };
 
+#ifndef FMHA_D64_EPI_WG
+#define FMHA_D64_EPI_WG 0  // measured slower (profiles/r02_microbench.txt): off
+#endif
+
 template <int D>
 struct FwdCfg {
   static_assert(D == 64 || D == 128, "this kernel handles head dim 64 and 128");
@@ -128,7 +132,18 @@ struct FwdCfg {
   static constexpr int kChunks = D / 64;  // 128-B swizzle atoms along d
   static constexpr int kQTileBytes = kBM * D * 2;
   static constexpr int kKVTileBytes = kBN * D * 2;
-  static constexpr int kStages = D == 64 ? 8 : 4;  // K/V ring depth
+  // Option (FMHA_D64_EPI_WG=1, d = 64): a dedicated epilogue warpgroup drains
+  // O (TMEM has room for two O buffers per Q tile, alternating per unit), so
+  // the softmax WGs go straight from a unit's last P to the next unit's first
+  // S.  Measured 6-8 % slower at N = 256..768: the 512-thread CTA caps the
+  // softmax WGs at 176 registers and their exponential phases slow down more
+  // than the epilogue overlap saves (profiles/r02_microbench.txt).
+  static constexpr bool kEpiWG = D == 64 && FMHA_D64_EPI_WG != 0;
+#ifdef FMHA_D64_STAGES
+  static constexpr int kStages = D == 64 ? FMHA_D64_STAGES : 4;
+#else
+  static constexpr int kStages = D == 64 ? (kEpiWG ? 7 : 8) : 4;  // K/V ring depth
+#endif
   static constexpr int kQStages = D == 64 ? 2 : 1;  // Q double-buffered when it fits
   static constexpr int kSmemQ = kQStages * 2 * kQTileBytes;
   // O staging for the TMA store: one tile per softmax WG when it fits (d = 64),
@@ -138,15 +153,23 @@ struct FwdCfg {
   static constexpr int kOBufs = D == 64 ? 2 : 1;
   static constexpr int kSmemO = kOBufs * kQTileBytes;
   static constexpr int kSmemRing = kStages * kKVTileBytes;
+  static constexpr int kSmemStats = kEpiWG ? 4 * kBM * 8 : 0;  // (m, Sigma) per row, per (tile, O buffer)
   static constexpr int kPChunks = 2;  // P published in two halves of 64 kv rows
-  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 8;
-  static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kNumBars * 8 + 16;
+  static constexpr int kOBar = kEpiWG ? 4 : 2;  // o_full / o_empty: per tile (x O buffer)
+  static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 2 * kPChunks + 2 * kOBar + 4 + (kEpiWG ? 4 : 0);
+  static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kSmemStats + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024-B alignment
-  static constexpr int kThreads = 384;  // 3 warpgroups: softmax 0, softmax 1, load/MMA
-  static constexpr int kLoadWarp = 8;
-  static constexpr int kMmaWarp = 9;
-  static constexpr int kStoreWarp = 10;
+  // 3 warpgroups: softmax 0, softmax 1, load/MMA/store (+ the epilogue WG at d = 64)
+  static constexpr int kThreads = kEpiWG ? 512 : 384;
+  static constexpr int kEpiWarp0 = 8;
+  static constexpr int kLoadWarp = kEpiWG ? 12 : 8;
+  static constexpr int kMmaWarp = kEpiWG ? 13 : 9;
+  static constexpr int kStoreWarp = kEpiWG ? 14 : 10;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
+  // O of tile q in buffer ob (ob = unit & 1 with the epilogue WG, else 0)
+  __host__ __device__ static constexpr uint32_t col_o(int q, int ob) {
+    return 256u + static_cast<uint32_t>(q * D + ob * 2 * D);
+  }
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kSeqBar = 1;  // named barriers 1, 2: exponential-phase turns of WG 0, 1
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
@@ -168,6 +191,10 @@ constexpr uint32_t kSoftmaxWaitNs = FMHA_PP_SOFTMAX_SLEEP_NS;
 #define FMHA_PP_STORE_SLEEP_NS 0  // O store warp: nanosleep between polls (measured -0.5 % at 256 ns)
 #endif
 constexpr uint32_t kStoreWaitNs = FMHA_PP_STORE_SLEEP_NS;
+#ifndef FMHA_EPI_SLEEP_NS
+#define FMHA_EPI_SLEEP_NS 64  // d = 64 epilogue WG: nanosleep between polls (off the critical path)
+#endif
+constexpr uint32_t kEpiSleepNs = FMHA_EPI_SLEEP_NS;
 #ifndef FMHA_KV_PREFETCH
 #define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
 #endif
@@ -204,7 +231,7 @@ __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int&
 
 // kEmuPer16: of every 16 score pairs, how many take the FMA-pipe exp2.
 template <int D, bool kBF16, int kEmuPer16 = 0>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
     fmha_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV,
@@ -217,18 +244,20 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQ = smem;
   uint8_t* sO = smem + C::kSmemQ;
   uint8_t* sRing = sO + C::kSmemO;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRing + C::kSmemRing + C::kSmemStats);
   uint64_t* q_full = bars;               // [kQStages]
   uint64_t* q_empty = bars + C::kQStages;  // [kQStages]
   uint64_t* kv_full = bars + 2 * C::kQStages;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;  // [2]
   uint64_t* p_full = s_full + 2;             // [2][kPChunks]: (tile q, chunk of kv rows)
-  uint64_t* o_full = p_full + 2 * C::kPChunks;  // [2]
-  uint64_t* o_empty = o_full + 2;            // [2]
-  uint64_t* stage_free = o_empty + 2;        // [2]: WG q's use of the O staging tile read by its TMA store
+  uint64_t* o_full = p_full + 2 * C::kPChunks;  // [kOBar]: tile q (x O buffer ob: index 2q + ob)
+  uint64_t* o_empty = o_full + C::kOBar;     // [kOBar]
+  uint64_t* stage_free = o_empty + C::kOBar;  // [2]: WG q's use of the O staging tile read by its TMA store
   uint64_t* stage_ready = stage_free + 2;    // [2] O staged (kOBufs == 2: per WG; else [0] in turns)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stage_ready + 2);
+  uint64_t* stat_full = stage_ready + 2;     // [4] (epilogue WG) unit's (m, Sigma) of tile q, buffer ob
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stat_full + (C::kEpiWG ? 4 : 0));
+  float2* stats = reinterpret_cast<float2*>(sRing + C::kSmemRing);  // [4][128] (epilogue WG)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -254,9 +283,13 @@ __global__ void __launch_bounds__(384, 1)
     for (int q = 0; q < 2; ++q) {
       mbar_init(&s_full[q], 1);
       for (int c = 0; c < C::kPChunks; ++c) mbar_init(&p_full[q * C::kPChunks + c], 128);  // every softmax thread
-      mbar_init(&o_full[q], 1);
-      mbar_init(&o_empty[q], 128);
     }
+    for (int t = 0; t < C::kOBar; ++t) {
+      mbar_init(&o_full[t], 1);
+      mbar_init(&o_empty[t], 128);
+    }
+    if constexpr (C::kEpiWG)
+      for (int t = 0; t < 4; ++t) mbar_init(&stat_full[t], 128);
     mbar_init(&stage_free[0], 1);
     mbar_init(&stage_free[1], 1);
     mbar_init(&stage_ready[0], 128);
@@ -268,6 +301,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // o_full / o_empty index of tile q, O buffer ob
+  auto oslot = [](int q, int ob) { return C::kEpiWG ? 2 * q + ob : q; };
 #ifdef FMHA_TRACE_BUILD
   if (threadIdx.x == 0 && tr) {
     args.trace[6] = t_start;
@@ -278,8 +313,43 @@ __global__ void __launch_bounds__(384, 1)
   // Register split (setmaxnreg inside each role's branch so ptxas sees one
   // limit per region): the load/MMA warpgroup needs few registers, the
   // softmax warpgroups hold a 128-column S row plus packed P per thread.
-  if (warp >= 8) {
-    reg_dealloc<112>();
+  if (C::kEpiWG && warp >= C::kEpiWarp0 && warp < C::kEpiWarp0 + 4) {
+    reg_dealloc<72>();
+    // ------------------------------------------- epilogue WG (d = 64) --
+    // rowwise_finalize (attention.cpp:68-73) + LSE for both Q tiles of every
+    // unit: O_q (TMEM buffer i & 1) x 1/Sigma -> 16-bit -> staging tile q ->
+    // TMA store by the store warp; one row per thread (lane quarter warp & 3).
+    const int r = (warp - C::kEpiWarp0) * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    int i = 0;
+    // the CTA's last unit is drained by the softmax WGs themselves (they are
+    // idle by then; two WGs in parallel keep the kernel's tail short)
+    const int last_u = args.n_units - 1 - (args.n_units - 1 - static_cast<int>(blockIdx.x)) % static_cast<int>(gridDim.x);
+    for (int u = blockIdx.x; u < last_u; u += gridDim.x, ++i) {
+      int b, head, qb;
+      decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+      const int ob = i & 1;
+      const uint32_t par = static_cast<uint32_t>(i >> 1) & 1;
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const int slot = 2 * q + ob;
+        mbar_wait_backoff(&o_full[slot], par, kEpiSleepNs);
+        mbar_wait_backoff(&stat_full[slot], par, kEpiSleepNs);
+        tc_fence_after();
+        const float2 st = stats[slot * C::kBM + r];
+        if (i > 0) mbar_wait_backoff(&stage_free[q], static_cast<uint32_t>(i - 1) & 1, kEpiSleepNs);
+        stage_o_tile<D, kBF16>(tmem + lane_off + C::col_o(q, ob), sO + q * C::kQTileBytes, r, 1.0f / st.y);
+        tc_fence_before();
+        fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
+        mbar_arrive(&o_empty[slot]);  // O buffer and statistics consumed
+        mbar_arrive(&stage_ready[q]);
+        const int row = qb * 2 * C::kBM + q * C::kBM + r;
+        if (row < args.n_q && args.lse != nullptr)
+          args.lse[(static_cast<int64_t>(b) * args.H + head) * args.N + row] = st.x * args.scale + logf(st.y);
+      }
+    }
+  } else if (warp >= 8) {
+    reg_dealloc<C::kEpiWG ? 88 : 112>();
     if (warp == C::kLoadWarp) {
       // -------------------------------------------------- TMA producer --
       if (lane == 0) {
@@ -381,6 +451,7 @@ __global__ void __launch_bounds__(384, 1)
       // A = P from TMEM (8 columns per step); B = V, MN-major (d contiguous):
       // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.  P arrives
       // in kPChunks chunks; each chunk's MMAs start as soon as it is stored.
+      int ob_cur = 0;  // O buffer of the current unit
       auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par, bool trp, int jt) {
         const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
         const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
@@ -398,7 +469,7 @@ __global__ void __launch_bounds__(384, 1)
           tc_fence_after();
 #pragma unroll
           for (int kk = c * kStepsPerChunk; kk < (c + 1) * kStepsPerChunk; ++kk)
-            mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,
+            mma_ts_elect(tmem + C::col_o(q, ob_cur), p0 + kk * 8,
                          sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
                          (accumulate || kk > 0) ? 1u : 0u);
         }
@@ -408,7 +479,11 @@ __global__ void __launch_bounds__(384, 1)
       int i = 0;
       for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
         const bool trm = tr && i == 0;
-        const uint32_t ue = (static_cast<uint32_t>(i) & 1) ^ 1;  // o_empty parity
+        // O buffer of this unit and the o_empty phase to wait for: the previous
+        // unit's epilogue (one buffer), or unit i-2's (epilogue WG, two buffers)
+        const int ob = C::kEpiWG ? (i & 1) : 0;
+        const uint32_t ue = C::kEpiWG ? ((static_cast<uint32_t>(i >> 1) & 1) ^ 1) : ((static_cast<uint32_t>(i) & 1) ^ 1);
+        ob_cur = ob;
         const int qs = i % C::kQStages;
         prof.mark(3);
         mbar_wait(&q_full[qs], static_cast<uint32_t>(i / C::kQStages) & 1);
@@ -434,7 +509,7 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t par = it & 1;
           if (j == 1) {  // previous unit's epilogue drained O0
             prof.mark(3);
-            mbar_wait(&o_empty[0], ue);
+            mbar_wait(&o_empty[oslot(0, ob)], ue);
             prof.mark(2);
           }
           mma_pv(0, vs, j > 1, par, trm, j - 1);
@@ -444,7 +519,7 @@ __global__ void __launch_bounds__(384, 1)
           trace_stamp(args, trm, 0, j - 1, 5);
           if (j == 1) {
             prof.mark(3);
-            mbar_wait(&o_empty[1], ue);
+            mbar_wait(&o_empty[oslot(1, ob)], ue);
             prof.mark(2);
           }
           mma_pv(1, vs, j > 1, par, trm, j - 1);
@@ -459,12 +534,12 @@ __global__ void __launch_bounds__(384, 1)
         }
         const int vs = next_slot();
         const uint32_t par = it & 1;
-        if (n_kv == 1) mbar_wait(&o_empty[0], ue);
+        if (n_kv == 1) mbar_wait(&o_empty[oslot(0, ob)], ue);
         mma_pv(0, vs, n_kv > 1, par, false, 0);
-        mma_commit_elect(&o_full[0]);
-        if (n_kv == 1) mbar_wait(&o_empty[1], ue);
+        mma_commit_elect(&o_full[oslot(0, ob)]);
+        if (n_kv == 1) mbar_wait(&o_empty[oslot(1, ob)], ue);
         mma_pv(1, vs, n_kv > 1, par, false, 0);
-        mma_commit_elect(&o_full[1]);
+        mma_commit_elect(&o_full[oslot(1, ob)]);
         mma_commit_elect(&kv_empty[vs]);
         ++it;
       }
@@ -501,13 +576,13 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else {
-    reg_alloc<192>();
+    reg_alloc<C::kEpiWG ? 176 : 192>();
     // ------------------------------------------------- softmax WG 0 / 1 --
     const int q = warp >> 2;
     const int r = threadIdx.x & 127;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_off + (q ? C::kColS1 : C::kColS0);
-    const uint32_t tO = tmem + lane_off + (q ? C::kColO1 : C::kColO0);
+    uint32_t tO = tmem + lane_off + C::col_o(q, 0);  // this unit's O_q (buffer i & 1 with the epilogue WG)
     const float sl2 = args.scale_log2;
     const int N = args.N;
     // shared-window barrier addresses, computed once (hot loop)
@@ -523,6 +598,7 @@ __global__ void __launch_bounds__(384, 1)
       int b, head, qb;
       decode_unit(u, args.n_qblocks, args.H, b, head, qb);
       const bool trq = tr && i == 0 && r == 0;
+      if constexpr (C::kEpiWG) tO = tmem + lane_off + C::col_o(q, i & 1);
       float m = -INFINITY;  // running max in raw score units
       float l = 0.0f;       // running sum of exp2((s - m) * sl2)
 
@@ -544,7 +620,10 @@ __global__ void __launch_bounds__(384, 1)
 #endif
         tc_fence_after();
         uint32_t sr[128];
-        tmem_ld32x32b_x128(tS, sr);
+        if constexpr (C::kThreads > 384)
+          tmem_ld32x32b_x64x2(tS, sr);  // base register budget 128: no 129-operand instruction
+        else
+          tmem_ld32x32b_x128(tS, sr);
         trace_stamp(args, trq, q, j, 1);
         float s[128];
 #pragma unroll
@@ -656,11 +735,24 @@ __global__ void __launch_bounds__(384, 1)
 #endif
       }
 
+      if (C::kEpiWG && u + static_cast<int>(gridDim.x) < args.n_units) {
+        // hand (m, Sigma) to the epilogue WG; the slot (tile q, buffer i & 1)
+        // was last read by unit i-2's epilogue (o_empty, as the MMA warp waits)
+        const int slot = 2 * q + (i & 1);
+        mbar_wait(&o_empty[slot], (static_cast<uint32_t>(i >> 1) & 1) ^ 1);
+        stats[slot * C::kBM + r] = make_float2(m, l);
+        mbar_arrive(&stat_full[slot]);
+        prof.mark(6);
+        continue;
+      }
       // ----------------------------------------------------- epilogue --
       // O_q -> registers -> x(1/Sigma) (rowwise_finalize) -> 16-bit -> the
       // swizzled staging tile -> TMA store; TMEM is released as soon as it
       // has been read so the next unit's first PV can start.
-      mbar_wait(&o_full[q], i & 1);
+      if constexpr (C::kEpiWG)
+        mbar_wait(&o_full[2 * q + (i & 1)], static_cast<uint32_t>(i >> 1) & 1);
+      else
+        mbar_wait(&o_full[q], i & 1);
       tc_fence_after();
       trace_stamp(args, trq, q, n_kv - 1, 6);
       // The two WGs take the staging tile in strict turns (WG0 unit i, WG1
@@ -680,7 +772,7 @@ __global__ void __launch_bounds__(384, 1)
       stage_o_tile<D, kBF16>(tO, stage, r, 1.0f / l);
       tc_fence_before();
       fence_proxy_async_smem();  // staged O visible to the TMA (async proxy)
-      mbar_arrive(&o_empty[q]);  // O_q drained from TMEM (all 128 threads)
+      mbar_arrive(&o_empty[C::kEpiWG ? 2 * q + (i & 1) : q]);  // O_q drained from TMEM (all 128 threads)
       mbar_arrive(&stage_ready[C::kOBufs == 2 ? q : 0]);  // this thread's row staged
       const int row = qb * 2 * C::kBM + q * C::kBM + r;
       if (row < args.n_q && args.lse != nullptr)
