@@ -195,6 +195,17 @@ constexpr uint32_t kStoreWaitNs = FMHA_PP_STORE_SLEEP_NS;
 #define FMHA_EPI_SLEEP_NS 64  // d = 64 epilogue WG: nanosleep between polls (off the critical path)
 #endif
 constexpr uint32_t kEpiSleepNs = FMHA_EPI_SLEEP_NS;
+// Register split of the 384-thread kernel.  The CTA launches with 168 per
+// thread (64512 in all); setmaxnreg.inc blocks until the dealloc'd registers
+// cover it, so 2 * softmax + role <= 3 * 168 = 504 (else: a hang).
+#ifndef FMHA_PP_SOFTMAX_REGS
+#define FMHA_PP_SOFTMAX_REGS 192
+#endif
+#ifndef FMHA_PP_ROLE_REGS
+#define FMHA_PP_ROLE_REGS 112
+#endif
+constexpr uint32_t kSoftmaxRegs = FMHA_PP_SOFTMAX_REGS, kRoleRegs = FMHA_PP_ROLE_REGS;
+static_assert(2 * FMHA_PP_SOFTMAX_REGS + FMHA_PP_ROLE_REGS <= 504, "setmaxnreg budget of the 384-thread CTA");
 #ifndef FMHA_KV_PREFETCH
 #define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
 #endif
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       }
     }
   } else if (warp >= 8) {
-    reg_dealloc<C::kEpiWG ? 88 : 112>();
+    reg_dealloc<C::kEpiWG ? 88 : kRoleRegs>();
     if (warp == C::kLoadWarp) {
       // -------------------------------------------------- TMA producer --
       if (lane == 0) {
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       }
     }
   } else {
-    reg_alloc<C::kEpiWG ? 176 : 192>();
+    reg_alloc<C::kEpiWG ? 176 : kSoftmaxRegs>();
     // ------------------------------------------------- softmax WG 0 / 1 --
     const int q = warp >> 2;
     const int r = threadIdx.x & 127;
