@@ -13,3 +13,4 @@ done
 python tools/exp/clock_under_load.py c3 c5 c4 c2 > gpurun_out/sustained.txt 2>&1; cat gpurun_out/sustained.txt
 make -s prof > /dev/null 2>&1; python tools/prof_phases.py > gpurun_out/phases_c3.txt 2>&1; python tools/prof_phases.py 16 12 512 64 > gpurun_out/phases_c2.txt 2>&1; cat gpurun_out/phases_c3.txt
 ls -la gpurun_out
+bash tools/exp/epi_probe.sh > gpurun_out/epilogue_probe.txt 2>&1; cat gpurun_out/epilogue_probe.txt
