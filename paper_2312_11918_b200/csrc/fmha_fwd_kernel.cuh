@@ -630,6 +630,18 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         if (tr && i < 8 && r == 0 && j == 0) args.trace[(3 * n_kv) * 16 + i * 8 + 1 + q] = clock64();
 #endif
         tc_fence_after();
+#ifdef FMHA_PROBE_ONE_WG
+        // probe build only (tools/prof_phases.py): WG 1 publishes P (garbage) at
+        // once, so WG 0's phase profile shows its softmax without a second
+        // softmax on its SM sub-partitions
+        if (q == 1) {
+          tc_fence_before();
+          mbar_arrive_addr(a_p_full0);
+          mbar_arrive_addr(a_p_full1);
+          prof.mark(5);
+          continue;
+        }
+#endif
         uint32_t sr[128];
         if constexpr (C::kThreads > 384)
           tmem_ld32x32b_x64x2(tS, sr);  // base register budget 128: no 129-operand instruction

@@ -37,3 +37,7 @@ print("softmax warps SMSP1:   " + "  ".join(f"{n} {x:6.0f}" for n, x in zip(name
 ld = acc[:, 8].mean(axis=0) / tiles_per_cta
 print(f"TMA producer:          wait kv_empty {ld[0]:6.0f}  other {ld[3]:6.0f}")
 print("MMA warp:              " + "  ".join(f"{n} {x:6.0f}" for n, x in zip(names_mma[:6], mma[:6])) + f"   total {mma[:6].sum():.0f}")
+wg0 = acc[:, 0:4].mean(axis=(0, 1)) / tiles_per_cta
+wg1 = acc[:, 4:8].mean(axis=(0, 1)) / tiles_per_cta
+print("softmax WG 0:          " + "  ".join(f"{n} {x:6.0f}" for n, x in zip(names_sm, wg0)) + f"   total {wg0.sum():.0f}")
+print("softmax WG 1:          " + "  ".join(f"{n} {x:6.0f}" for n, x in zip(names_sm, wg1)) + f"   total {wg1.sum():.0f}")
