@@ -448,15 +448,15 @@ __global__ void __launch_bounds__(512, 1)
         // s[4c .. 4c+3]: group c (kv columns 8c + 2*quad + {0,1}) of rows r0, r0 + 8
         float s[64];
         // row maxima of groups [c0, c1) into (mx0, mx1), before the quad reduction
-        auto group_max = [&](int c0, int c1, float& mx0, float& mx1) {
-          float a0 = fmaxf(s[4 * c0], s[4 * c0 + 1]), a1 = fmaxf(s[4 * c0 + 2], s[4 * c0 + 3]);
-          float b0 = fmaxf(s[4 * c0 + 4], s[4 * c0 + 5]), b1 = fmaxf(s[4 * c0 + 6], s[4 * c0 + 7]);
+        auto group_max = [](const float (&v)[64], int c0, int c1, float& mx0, float& mx1) {
+          float a0 = fmaxf(v[4 * c0], v[4 * c0 + 1]), a1 = fmaxf(v[4 * c0 + 2], v[4 * c0 + 3]);
+          float b0 = fmaxf(v[4 * c0 + 4], v[4 * c0 + 5]), b1 = fmaxf(v[4 * c0 + 6], v[4 * c0 + 7]);
 #pragma unroll
           for (int c = c0 + 2; c < c1; c += 2) {
-            a0 = fmaxf(a0, fmaxf(s[4 * c], s[4 * c + 1]));
-            a1 = fmaxf(a1, fmaxf(s[4 * c + 2], s[4 * c + 3]));
-            b0 = fmaxf(b0, fmaxf(s[4 * c + 4], s[4 * c + 5]));
-            b1 = fmaxf(b1, fmaxf(s[4 * c + 6], s[4 * c + 7]));
+            a0 = fmaxf(a0, fmaxf(v[4 * c], v[4 * c + 1]));
+            a1 = fmaxf(a1, fmaxf(v[4 * c + 2], v[4 * c + 3]));
+            b0 = fmaxf(b0, fmaxf(v[4 * c + 4], v[4 * c + 5]));
+            b1 = fmaxf(b1, fmaxf(v[4 * c + 6], v[4 * c + 7]));
           }
           mx0 = fmaxf(a0, b0);
           mx1 = fmaxf(a1, b1);
@@ -526,11 +526,11 @@ __global__ void __launch_bounds__(512, 1)
           dbs_stamp(args, tr && threadIdx.x == 0, g, 1);
           exp_half.template operator()<kEmuPer16>(0, ph0);
           float ma0, ma1, mb0, mb1;
-          group_max(0, 8, ma0, ma1);
+          group_max(s, 0, 8, ma0, ma1);
           tmem_wait_ld();
 #pragma unroll
           for (int k = 0; k < 32; ++k) s[32 + k] = __uint_as_float(srb[k]);
-          group_max(8, 16, mb0, mb1);
+          group_max(s, 8, 16, mb0, mb1);
           float mx0 = fmaxf(ma0, mb0), mx1 = fmaxf(ma1, mb1);
           quad_max(mx0, mx1);
           dbs_stamp(args, tr && threadIdx.x == 0, g, 2);
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(512, 1)
               if ((k >> 2) * 8 + 2 * quad + (k & 1) >= valid) s[k] = -INFINITY;
           }
           float mx0, mx1;
-          group_max(0, 16, mx0, mx1);
+          group_max(s, 0, 16, mx0, mx1);
           quad_max(mx0, mx1);
           if (grew(mx0, mx1)) raise_max(mx0, mx1);
           dbs_stamp(args, tr && threadIdx.x == 0, g, 2);
