@@ -40,6 +40,10 @@
 
 namespace fmha_b200 {
 
+#ifndef FMHA_SPLIT_SHARED
+#define FMHA_SPLIT_SHARED 0
+#endif
+
 template <int D>
 struct SplitCfg {
   static_assert(D == 64 || D == 128, "this kernel handles head dim 64 and 128");
@@ -59,9 +63,14 @@ struct SplitCfg {
   static constexpr int kNumBars = 2 * kQStages + 2 * kStages + 2 + 4 + 2 + 2 + 2;
   static constexpr int kSmemBytes = kSmemQ + kSmemO + kSmemRing + kSmemRed + kNumBars * 8 + 16;
   static constexpr int kSmemAlloc = kSmemBytes + 1024;
-  static constexpr int kThreads = 576;
-  static constexpr int kLoadWarp = 16;
-  static constexpr int kMmaWarp = 17;
+  // FMHA_SPLIT_SHARED: EIGHT softmax warps, each serving BOTH Q tiles (tile 0's
+  // half-rows, then tile 1's, every K/V step), so a tile's exponentials run on
+  // two warps of each sub-partition with the whole MUFU to themselves.
+  static constexpr bool kShared = FMHA_SPLIT_SHARED != 0;
+  static constexpr int kSoftmaxWarps = kShared ? 8 : 16;
+  static constexpr int kThreads = kShared ? 320 : 576;
+  static constexpr int kLoadWarp = kSoftmaxWarps;
+  static constexpr int kMmaWarp = kSoftmaxWarps + 1;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kPairBar = 1;   // named barriers 1..8: (q, k) partner pairs, 64 threads
@@ -73,7 +82,7 @@ template <int D, bool kBF16, int kEmuPer16>
 // 576 threads: each SM sub-partition's 16K-register file holds up to 5 warps
 // (sub-partitions 0 and 1: four softmax warps + the load / MMA warp), so 96
 // registers per thread; the exponentials go in two 32-column chunks to fit.
-__global__ void __launch_bounds__(576, 1)
+__global__ void __launch_bounds__(SplitCfg<D>::kThreads, 1)
     fmha_fwd_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                           const FwdArgs args) {
@@ -256,6 +265,148 @@ __global__ void __launch_bounds__(576, 1)
       mma_commit_elect(&kv_empty[vs]);
       ++it;
     }
+  } else if constexpr (C::kShared) {
+    // ------------------------------------------ softmax (8 shared warps) --
+    // warp w: TMEM lane quarter k = w & 3, score columns [64c, 64c + 64) with
+    // c = w >> 2, for BOTH Q tiles: per K/V step tile 0's half-rows, then tile
+    // 1's.  Partner warp w ^ 4 holds the other 64 columns of the same rows.
+    const int k = warp & 3;
+    const int c = warp >> 2;
+    const int r = k * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(k * 32) << 16;
+    constexpr int kOC = D / 2;
+    const float sl2 = args.scale_log2;
+    const int N = args.N;
+    const uint32_t pair_bar = C::kPairBar + k;
+    float* red_mine = sRed + c * 256 + r;
+    const float* red_other = sRed + (c ^ 1) * 256 + r;
+    uint32_t e = 0;
+    auto exchange = [&](float x) {
+      red_mine[(e & 1) * 128] = x;
+      named_bar_sync(pair_bar, 64);
+      const float y = red_other[(e & 1) * 128];
+      ++e;
+      return y;
+    };
+    uint32_t it = 0;
+    int i = 0;
+    for (int u = blockIdx.x; u < args.n_units; u += gridDim.x, ++i) {
+      int b, head, qb;
+      decode_unit(u, args.n_qblocks, args.H, b, head, qb);
+      float m[2] = {-INFINITY, -INFINITY};  // running row max per tile (identical in both warps of a pair)
+      float l[2] = {0.0f, 0.0f};            // partial running sums over this warp's columns
+      for (int j = 0; j < n_kv; ++j, ++it) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t tS = tmem + lane_off + (q ? C::kColS1 : C::kColS0);
+          const uint32_t tSc = tS + 64 * c, tPc = tS + 32 * c;
+          const uint32_t tOc = tmem + lane_off + (q ? C::kColO1 : C::kColO0) + kOC * c;
+          mbar_wait(&s_full[q], it & 1);
+          tc_fence_after();
+          uint32_t sr[64];
+          tmem_ld32x32b_x64(tSc, sr);
+          float s[64];
+#pragma unroll
+          for (int t = 0; t < 64; ++t) s[t] = __uint_as_float(sr[t]);
+          const int valid = N - j * C::kBN - 64 * c;
+          if (valid < 64) {
+#pragma unroll
+            for (int t = 0; t < 64; ++t)
+              if (t >= valid) s[t] = -INFINITY;
+          }
+          float mx;
+          {
+            float a[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) a[t] = fmaxf(s[t], s[t + 4]);
+#pragma unroll
+            for (int t = 8; t < 64; t += 8)
+#pragma unroll
+              for (int x = 0; x < 4; ++x) a[x] = fmaxf(a[x], fmaxf(s[t + x], s[t + x + 4]));
+            mx = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3]));
+          }
+          mx = fmaxf(mx, exchange(mx));
+          if (__any_sync(0xffffffffu, (mx - m[q]) * sl2 > 8.0f)) {
+            const float m_new = fmaxf(mx, m[q]);
+            if (j > 0) {  // O_q quiescent: S_q(j) observed => PV_q(j-1) done
+              const float alpha = ex2_approx((m[q] - m_new) * sl2);
+              l[q] *= alpha;
+#pragma unroll
+              for (int cc = 0; cc < kOC / 16; ++cc) {
+                uint32_t o[16];
+                tmem_ld32x32b_x16(tOc + cc * 16, o);
+#pragma unroll
+                for (int t = 0; t < 16; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+                tmem_st32x32b_x16(tOc + cc * 16, o);
+              }
+            }
+            m[q] = m_new;
+          }
+          const float neg = -m[q] * sl2;
+          uint32_t p0[16], p1[16];
+          float rs;
+          if (valid < 64) {
+            rs = exp_rowsum_pack<kBF16, 0, 32, 0>(s, sl2, neg, p0);
+            tmem_st32x32b_x16(tPc, p0);
+            rs += exp_rowsum_pack<kBF16, 32, 32, 0>(s, sl2, neg, p1);
+          } else {
+            rs = exp_rowsum_pack<kBF16, 0, 32, kEmuPer16>(s, sl2, neg, p0);
+            tmem_st32x32b_x16(tPc, p0);
+            rs += exp_rowsum_pack<kBF16, 32, 32, kEmuPer16>(s, sl2, neg, p1);
+          }
+          tmem_st32x32b_x16(tPc + 16, p1);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&p_full[2 * q + c]);
+          l[q] += rs;
+        }
+      }
+      // ------------------------------------------------------- epilogue --
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const float l_tot = l[q] + exchange(l[q]);
+        mbar_wait(&o_full[q], i & 1);
+        tc_fence_after();
+        if (q == 1)
+          mbar_wait(&stage_free[0], static_cast<uint32_t>(i) & 1);
+        else if (i > 0)
+          mbar_wait(&stage_free[1], static_cast<uint32_t>(i - 1) & 1);
+        const float inv = 1.0f / l_tot;
+        const uint32_t tOc = tmem + lane_off + (q ? C::kColO1 : C::kColO0) + kOC * c;
+#pragma unroll
+        for (int cc = 0; cc < kOC / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32x32b_x32(tOc + cc * 32, o);
+          uint32_t h2[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            h2[t] = pack2<kBF16>(__uint_as_float(o[2 * t]) * inv, __uint_as_float(o[2 * t + 1]) * inv);
+          const int col = kOC * c + 32 * cc;
+          uint8_t* rowp = sO + (col >> 6) * (C::kBM * 128) + r * 128;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int unit = (((col & 63) >> 3) + v) ^ (r & 7);  // 128-B swizzle
+            st_shared_v4(rowp + unit * 16, h2[4 * v], h2[4 * v + 1], h2[4 * v + 2], h2[4 * v + 3]);
+          }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        mbar_arrive(&o_empty[q]);               // O_q drained from TMEM (256 arrivals)
+        named_bar_sync(C::kTileBar, 256);       // all 8 warps have staged their columns
+        if (warp == 0 && lane == 0) {
+#pragma unroll
+          for (int cc = 0; cc < C::kChunks; ++cc)
+            tma_store_4d(&tmO, sO + cc * C::kBM * 128, cc * 64, head, qb * 2 * C::kBM + q * C::kBM, b);
+          tma_store_commit();
+          tma_store_wait_read();
+          mbar_arrive(&stage_free[q]);
+        }
+        const int row = qb * 2 * C::kBM + q * C::kBM + r;
+        if (c == 0 && row < args.n_q && args.lse != nullptr)
+          args.lse[(static_cast<int64_t>(b) * args.H + head) * N + row] = m[q] * args.scale + logf(l_tot);
+      }
+    }
+    if (warp == 0 && lane == 0) tma_store_wait_all();
   } else {
     // --------------------------------------------------------- softmax --
     const int k = warp & 3;
