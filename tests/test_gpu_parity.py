@@ -273,10 +273,12 @@ def test_pair_kernel_matches_single_cta_kernel_bitwise(oracle, tmp_path):
     np.testing.assert_array_equal(lse.cpu().numpy(), ref["lse"])
 
 
+@pytest.mark.parametrize("env", ["FMHA_TUNE_DBS", "FMHA_TUNE_SPLIT"])
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
-def test_double_buffered_s_kernel_against_oracle(oracle, tmp_path, dt):
-    """The opt-in d = 128 double-buffered-S kernel (FMHA_TUNE_DBS=1, read once
-    per process, so it runs in a subprocess) against the oracle: ragged N
+def test_opt_in_d128_kernels_against_oracle(oracle, tmp_path, dt, env):
+    """The opt-in d = 128 kernels -- double-buffered S (FMHA_TUNE_DBS=1) and the
+    split-row ping-pong (FMHA_TUNE_SPLIT=1); read once per process, so they
+    run in a subprocess -- against the oracle: ragged N
     (masked last K/V step, TMA-clipped Q rows), several units per CTA (the
     flat step sequence crosses unit boundaries with an odd step count), and
     keys growing along the sequence, which force conditional O rescales in
@@ -303,12 +305,12 @@ def test_double_buffered_s_kernel_against_oracle(oracle, tmp_path, dt):
         f"    z = np.load({str(tmp_path)!r} + f'/in{{n}}.npz')\n"
         "    q, k, v = (torch.from_numpy(z[x]).cuda().to(td) for x in ('q', 'k', 'v'))\n"
         "    L, N, h, d = q.shape[0], q.shape[1], q.shape[2], q.shape[3]\n"
-        "    assert 'double-buffered' in fm.kernel_for(L, N, h, d, fm.BF16 if td == torch.bfloat16 else fm.F16)\n"
+        f"    assert {env!r} != 'FMHA_TUNE_DBS' or 'double-buffered' in fm.kernel_for(L, N, h, d, fm.BF16 if td == torch.bfloat16 else fm.F16)\n"
         "    o, lse = fm.fmha_fwd(q, k, v)\n"
         f"    np.savez({str(tmp_path)!r} + f'/out{{n}}.npz', o=o.float().cpu().numpy(), lse=lse.cpu().numpy())\n")
-    env = dict(os.environ, FMHA_TUNE_DBS="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=600)
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **{env: "1"}), cwd=root,
+                   timeout=600)
     for n, (L, N, h, s) in enumerate(cases):
         q, k, v = probs[n]
         out = np.load(tmp_path / f"out{n}.npz")
@@ -319,9 +321,9 @@ def test_double_buffered_s_kernel_against_oracle(oracle, tmp_path, dt):
                 r0, r1 = t * 128, min(N, t * 128 + 128)
                 res = errors(out["o"][b, r0:r1, hh], out["lse"][b, hh, r0:r1], o_ref[ti][: r1 - r0],
                              lse_ref[ti][: r1 - r0])
-                assert_within(res, f"dbs {dt} L={L} N={N} h={h} tile {(b, hh, t)}")
+                assert_within(res, f"{env} {dt} L={L} N={N} h={h} tile {(b, hh, t)}")
         else:
             bm = 128 if N % 128 == 0 else N
             o_ref, lse_ref = oracle.fmha_forward(q, k, v, bm, bm)
             res = errors(out["o"], out["lse"], o_ref, lse_ref)
-            assert_within(res, f"dbs {dt} L={L} N={N} h={h} scale {s}")
+            assert_within(res, f"{env} {dt} L={L} N={N} h={h} scale {s}")
