@@ -206,6 +206,10 @@ constexpr uint32_t kEpiSleepNs = FMHA_EPI_SLEEP_NS;
 #endif
 constexpr uint32_t kSoftmaxRegs = FMHA_PP_SOFTMAX_REGS, kRoleRegs = FMHA_PP_ROLE_REGS;
 static_assert(2 * FMHA_PP_SOFTMAX_REGS + FMHA_PP_ROLE_REGS <= 504, "setmaxnreg budget of the 384-thread CTA");
+#ifndef FMHA_UNIT_PREFETCH_MAX_KV
+#define FMHA_UNIT_PREFETCH_MAX_KV 0  // next-unit L2 prefetch for units of <= this many K/V steps (measured slower: off)
+#endif
+constexpr int kUnitPrefetchMaxKv = FMHA_UNIT_PREFETCH_MAX_KV;
 #ifndef FMHA_KV_PREFETCH
 #define FMHA_KV_PREFETCH 0  // K/V tiles prefetched into L2 this many steps ahead (0: off)
 #endif
@@ -378,6 +382,24 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           int b, head, qb;
           decode_unit(u, args.n_qblocks, args.H, b, head, qb);
           const int qrow0 = qb * 2 * C::kBM;
+          // Short units (few K/V steps): pull the CTA's NEXT unit's Q and K/V
+          // into L2 now, so only each CTA's first unit waits on HBM latency
+          // (with a cold L2 the loads at every unit start are latency-bound).
+          if (n_kv <= kUnitPrefetchMaxKv && u + static_cast<int>(gridDim.x) < args.n_units) {
+            int b2, head2, qb2;
+            decode_unit(u + gridDim.x, args.n_qblocks, args.H, b2, head2, qb2);
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c) {
+              tma_prefetch_4d(&tmQ, c * 64, head2, qb2 * 2 * C::kBM, b2);
+              tma_prefetch_4d(&tmQ, c * 64, head2, qb2 * 2 * C::kBM + C::kBM, b2);
+            }
+            for (int j = 0; j < n_kv; ++j)
+#pragma unroll
+              for (int c = 0; c < C::kChunks; ++c) {
+                tma_prefetch_4d(&tmK, c * 64, head2, j * C::kBN, b2);
+                tma_prefetch_4d(&tmV, c * 64, head2, j * C::kBN, b2);
+              }
+          }
           // Q stage is free once the last S GEMMs of the unit that used it
           // before have completed
           const int qs = i % C::kQStages;
