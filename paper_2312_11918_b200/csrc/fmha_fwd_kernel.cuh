@@ -206,6 +206,10 @@ constexpr uint32_t kEpiSleepNs = FMHA_EPI_SLEEP_NS;
 #endif
 constexpr uint32_t kSoftmaxRegs = FMHA_PP_SOFTMAX_REGS, kRoleRegs = FMHA_PP_ROLE_REGS;
 static_assert(2 * FMHA_PP_SOFTMAX_REGS + FMHA_PP_ROLE_REGS <= 504, "setmaxnreg budget of the 384-thread CTA");
+#ifndef FMHA_PP_SPLIT_S
+#define FMHA_PP_SPLIT_S 0  // S_q(j+1)'s upper 64 columns issued between PV_q(j)'s two P halves
+#endif
+constexpr bool kSplitS = FMHA_PP_SPLIT_S != 0;
 #ifndef FMHA_UNIT_PREFETCH_MAX_KV
 #define FMHA_UNIT_PREFETCH_MAX_KV 0  // next-unit L2 prefetch for units of <= this many K/V steps (measured slower: off)
 #endif
@@ -480,12 +484,29 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
                        sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
+      // Half of S_q = Q_q K^T: N = 64 kv rows [64h, 64h + 64) into S columns
+      // [64h, 64h + 64) (FMHA_PP_SPLIT_S: the upper half of S_q(j+1) is issued
+      // between the two P halves of PV_q(j) -- those columns no longer hold
+      // anything the softmax or GEMM-II still needs once P half 0 is published --
+      // so only the lower half (which P_q(j) occupies) waits for PV_q(j)).
+      constexpr uint32_t kIdescQK64 = idesc_f16(kBF16, C::kBM, 64, false, false);
+      auto mma_qk_half = [&](int q, int kslot, int h) {
+        const uint32_t a0 = sQ_addr + q * C::kQTileBytes;
+        const uint32_t b0 = ring_addr + kslot * C::kKVTileBytes + h * 64 * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
+          const uint32_t off_b = (kk >> 2) * (C::kBN * 128) + (kk & 3) * 32;
+          mma_ss_elect(tmem + (q ? C::kColS1 : C::kColS0) + 64 * h, sdesc_sw128(a0 + off_a, 16, 1024),
+                       sdesc_sw128(b0 + off_b, 16, 1024), kIdescQK64, kk > 0 ? 1u : 0u);
+        }
+      };
       // O_q (+)= P_q V : M=128, N=D, K=128 kv rows in 8 steps of 16 rows.
       // A = P from TMEM (8 columns per step); B = V, MN-major (d contiguous):
       // LBO = chunk stride along d, SBO = 1024 B per 8 kv rows.  P arrives
       // in kPChunks chunks; each chunk's MMAs start as soon as it is stored.
       int ob_cur = 0;  // O buffer of the current unit
-      auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par, bool trp, int jt) {
+      auto mma_pv = [&](int q, int vslot, bool accumulate, uint32_t par, bool trp, int jt, int ks_hi = -1) {
         const uint32_t b0 = ring_addr + vslot * C::kKVTileBytes;
         const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
         constexpr int kStepsPerChunk = 8 / C::kPChunks;
@@ -505,6 +526,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             mma_ts_elect(tmem + C::col_o(q, ob_cur), p0 + kk * 8,
                          sdesc_sw128(b0 + kk * 16 * 128, C::kBN * 128, 1024), kIdescPV,
                          (accumulate || kk > 0) ? 1u : 0u);
+          if (c == 0 && ks_hi >= 0) mma_qk_half(q, ks_hi, 1);
         }
       };
 
@@ -545,9 +567,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             mbar_wait(&o_empty[oslot(0, ob)], ue);
             prof.mark(2);
           }
-          mma_pv(0, vs, j > 1, par, trm, j - 1);
-          trace_stamp(args, trm, 0, j - 1, 12);
-          mma_qk(0, ks);
+          if constexpr (kSplitS) {
+            mma_pv(0, vs, j > 1, par, trm, j - 1, ks);
+            mma_qk_half(0, ks, 0);
+          } else {
+            mma_pv(0, vs, j > 1, par, trm, j - 1);
+            trace_stamp(args, trm, 0, j - 1, 12);
+            mma_qk(0, ks);
+          }
           mma_commit_elect(&s_full[0]);
           trace_stamp(args, trm, 0, j - 1, 5);
           if (j == 1) {
@@ -555,9 +582,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
             mbar_wait(&o_empty[oslot(1, ob)], ue);
             prof.mark(2);
           }
-          mma_pv(1, vs, j > 1, par, trm, j - 1);
-          trace_stamp(args, trm, 1, j - 1, 12);
-          mma_qk(1, ks);
+          if constexpr (kSplitS) {
+            mma_pv(1, vs, j > 1, par, trm, j - 1, ks);
+            mma_qk_half(1, ks, 0);
+          } else {
+            mma_pv(1, vs, j > 1, par, trm, j - 1);
+            trace_stamp(args, trm, 1, j - 1, 12);
+            mma_qk(1, ks);
+          }
           mma_commit_elect(&s_full[1]);
           trace_stamp(args, trm, 1, j - 1, 5);
           if (j == n_kv - 1) mma_commit_elect(&q_empty[qs]);  // last reads of Q issued
