@@ -460,6 +460,7 @@ struct Tuning {
   int split;  // split-row ping-pong for d <= 128 (FMHA_TUNE_SPLIT)
   int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N)
   int dbs;                // d = 128 below pair128_min_n: double-buffered-S kernel (FMHA_TUNE_DBS)
+  int emu64d;             // exp2 split of the two-CTA d = 64 kernel (FMHA_TUNE_EMU64D)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -469,7 +470,7 @@ const Tuning& tuning() {
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
                   env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
-                  env("FMHA_TUNE_DBS", 0)};
+                  env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4)};
   }();
   return t;
 }
@@ -603,6 +604,14 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       CUtensorMap mk64, mv64;
       if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
         return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (d=64 K/V maps)");
+      // exp2 split of the two-CTA d=64 kernel: FMHA_TUNE_EMU64D (A/B runs), default 4/16
+      const int e = tuning().emu64d;
+      if (e == 6)
+        return bf ? launch_d64<true, 6>(p, mq, mk64, mv64, mo, o, lse, st, nq)
+                  : launch_d64<false, 6>(p, mq, mk64, mv64, mo, o, lse, st, nq);
+      if (e == 8)
+        return bf ? launch_d64<true, 8>(p, mq, mk64, mv64, mo, o, lse, st, nq)
+                  : launch_d64<false, 8>(p, mq, mk64, mv64, mo, o, lse, st, nq);
       return bf ? launch_d64<true, 4>(p, mq, mk64, mv64, mo, o, lse, st, nq)
                 : launch_d64<false, 4>(p, mq, mk64, mv64, mo, o, lse, st, nq);
     }
