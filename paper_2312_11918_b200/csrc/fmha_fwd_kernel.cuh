@@ -206,6 +206,10 @@ constexpr uint32_t kEpiSleepNs = FMHA_EPI_SLEEP_NS;
 #endif
 constexpr uint32_t kSoftmaxRegs = FMHA_PP_SOFTMAX_REGS, kRoleRegs = FMHA_PP_ROLE_REGS;
 static_assert(2 * FMHA_PP_SOFTMAX_REGS + FMHA_PP_ROLE_REGS <= 504, "setmaxnreg budget of the 384-thread CTA");
+#ifndef FMHA_PP_LATE_SUM
+#define FMHA_PP_LATE_SUM 0  // row sum of P taken after P is published (off the S -> P chain)
+#endif
+constexpr bool kLateSum = FMHA_PP_LATE_SUM != 0;
 #ifndef FMHA_PP_SPLIT_S
 #define FMHA_PP_SPLIT_S 0  // S_q(j+1)'s upper 64 columns issued between PV_q(j)'s two P halves
 #endif
@@ -779,6 +783,21 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           }
         }
         prof.mark(2);
+        if (kLateSum && !kSpec) {
+          neg = -m * sl2;
+          if (masked)
+            exp_pack_inplace<kBF16, 0, 64, 0>(s, sl2, neg, p0);
+          else
+            exp_pack_inplace<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+          trace_stamp(args, trq, q, j, 9);
+          prof.mark(3);
+          tmem_st32x32b_x32(tS, p0);
+          if (masked)
+            exp_pack_inplace<kBF16, 64, 64, 0>(s, sl2, neg, p1);
+          else
+            exp_pack_inplace<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+          rs = 0.0f;  // the row sum follows the publication below
+        } else {
         if (redo) {
           neg = -m * sl2;
           rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
@@ -789,6 +808,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         tmem_st32x32b_x32(tS, p0);
         rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
                      : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        }
         if constexpr (kSeq) named_bar_arrive(C::kSeqBar + (q ^ 1), 256);
         prof.mark(4);
         trace_stamp(args, trq, q, j, 10);
@@ -803,6 +823,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         trace_stamp(args, trq, q, j, 2);
         tmem_st32x32b_x32(tS + 32, p1);
         publish(1);
+        if constexpr (kLateSum && !kSpec) rs = row_sum_f32(s);  // off the S -> P path
         l += rs;
         prof.mark(5);
         trace_stamp(args, trq, q, j, 3);

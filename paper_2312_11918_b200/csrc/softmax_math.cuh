@@ -137,6 +137,41 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
   return (a0 + b0) + (a1 + b1);
 }
 
+// P only (no row sum): the kCols exponentials replace their scores in s
+// (fp32, unrounded) and are packed to 16-bit pairs; the row sum is taken
+// later with row_sum_f32, AFTER P has been published -- the FADD2 chain then
+// leaves the S -> P critical path (FlashAttention-4 orders it the same way).
+template <bool kBF16, int kOff, int kCols, int kEmuPer16, int kTotal>
+__device__ __forceinline__ void exp_pack_inplace(float (&s)[kTotal], float c, float neg_mc,
+                                                 uint32_t (&p)[kCols / 2]) {
+  const uint64_t c2 = f2_pack(c, c);
+  const uint64_t nm2 = f2_pack(neg_mc, neg_mc);
+#pragma unroll
+  for (int i = 0; i < kCols / 2; ++i) {
+    const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
+    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    f2_unpack(e, s[kOff + 2 * i], s[kOff + 2 * i + 1]);
+    p[i] = pack2_x2<kBF16>(e);
+  }
+}
+// fp32 sum of s[0, kTotal) with eight packed accumulators (short dependency chains)
+template <int kTotal>
+__device__ __forceinline__ float row_sum_f32(const float (&s)[kTotal]) {
+  uint64_t acc[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) acc[t] = f2_pack(s[2 * t], s[2 * t + 1]);
+#pragma unroll
+  for (int i = 8; i < kTotal; i += 8)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[t] = fadd2(acc[t], f2_pack(s[i + 2 * t], s[i + 2 * t + 1]));
+  acc[0] = fadd2(acc[0], acc[1]);
+  acc[2] = fadd2(acc[2], acc[3]);
+  acc[0] = fadd2(acc[0], acc[2]);
+  float a, b;
+  f2_unpack(acc[0], a, b);
+  return a + b;
+}
+
 // exp_rowsum_pack over s[0, 64) with the full 128-column row max of s
 // folded into the same instruction stream (FMNMX3 on the ALU pipe fills the
 // MUFU / FMA latency slots): the speculative form of a tile's first half,
