@@ -654,6 +654,9 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       if (emu == 8)
         return bf ? launch_d128<128, true, 8>(p, mq, mk, mv, mo, lse, st, nq)
                   : launch_d128<128, false, 8>(p, mq, mk, mv, mo, lse, st, nq);
+      if (emu == fmha_b200::kEmuEdgeFree)
+        return bf ? launch_d128<128, true, fmha_b200::kEmuEdgeFree>(p, mq, mk, mv, mo, lse, st, nq)
+                  : launch_d128<128, false, fmha_b200::kEmuEdgeFree>(p, mq, mk, mv, mo, lse, st, nq);
       return bf ? launch_d128<128, true, 4>(p, mq, mk, mv, mo, lse, st, nq)
                 : launch_d128<128, false, 4>(p, mq, mk, mv, mo, lse, st, nq);
     }

@@ -112,6 +112,22 @@ __device__ __forceinline__ constexpr bool emulate_pair(int i) {
 #endif
 }
 
+// kEmuPer16 == kEmuEdgeFree selects a position-dependent pattern over the
+// 128-score row (64 pairs in four 16-pair fragments): fragments 0 and 3 stay
+// all-MUFU (the first MUFU results are not held up by polynomial chains, the
+// last P fragment is not delayed by one), fragments 1 and 2 emulate 6 of 16
+// pairs -- 12 of 64 in all (FlashAttention-4's default split for d = 128).
+constexpr int kEmuEdgeFree = 17;
+template <int kEmuPer16>
+__device__ __forceinline__ constexpr bool emulate_pair_at(int ip) {
+  if constexpr (kEmuPer16 == kEmuEdgeFree) {
+    const int f = ip / 16, k2 = 2 * (ip % 16);
+    return f >= 1 && f <= 2 && k2 % 10 >= 6;
+  } else {
+    return emulate_pair<kEmuPer16>(ip);
+  }
+}
+
 // P = 2^(s*c - m*c) for the kCols scores s[kOff .. kOff+kCols) of one row;
 // returns the fp32 sum of the UNROUNDED P (attention.cpp:50-55) and writes
 // the 16-bit packed P.  Pairs selected by emulate_pair use the polynomial.
@@ -124,7 +140,8 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
 #pragma unroll
   for (int i = 0; i < kCols / 2; ++i) {
     const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
-    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    const bool emu = kEmuPer16 == kEmuEdgeFree ? emulate_pair_at<kEmuPer16>(kOff / 2 + i) : emulate_pair<kEmuPer16>(i);
+    const uint64_t e = emu ? exp2_poly_x2(x) : exp2_mufu_x2(x);
     if (i & 1)
       acc1 = fadd2(acc1, e);
     else
