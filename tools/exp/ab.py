@@ -21,7 +21,7 @@ for (L, h, N, d, dt) in shapes:
     g = torch.Generator(device="cuda").manual_seed(1234)
     q, k, v = (torch.randn(L, N, h, d, device="cuda", dtype=dt, generator=g) for _ in range(3))
     o = fm.fmha_fwd(q, k, v)[0]
-    key = f"/tmp/ab_ref_{L}_{h}_{N}_{d}.pt"
+    key = f"/tmp/ab_ref_{L}_{h}_{N}_{d}_{str(dt)[6:]}.pt"
     if tag == "base":
         torch.save(o.cpu(), key)
         diff = 0.0
