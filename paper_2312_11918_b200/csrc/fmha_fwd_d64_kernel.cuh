@@ -58,6 +58,11 @@ struct FwdCfgD64 {
   static_assert(kSmemAlloc <= 112 * 1024, "two CTAs per SM");
 };
 
+#ifndef FMHA_D64_K4
+#define FMHA_D64_K4 1  // batched tcgen05 issue (four K-steps per elect.sync): +1.5 % on Table-1 d=64
+#endif
+constexpr bool kD64K4 = FMHA_D64_K4 != 0;
+
 template <bool kBF16, int kEmuPer16 = 4>
 __global__ void __launch_bounds__(320, 2)
     fmha_fwd_d64_kernel(const __grid_constant__ CUtensorMap tmQ,  // box 128 rows
@@ -167,6 +172,11 @@ __global__ void __launch_bounds__(320, 2)
     auto mma_qk = [&](int q, int kslot) {
       const uint32_t a0 = sQ_addr + q * C::kQTileBytes;
       const uint32_t b0 = ring_addr + kslot * C::kKVTileBytes;
+      if constexpr (kD64K4) {  // the four K-steps in one elect.sync batch
+        mma_ss_k4(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0, 16, 1024), sdesc_sw128(b0, 16, 1024),
+                  kIdescQK, 0u);
+        return;
+      }
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         mma_ss_elect(tmem + (q ? C::kColS1 : C::kColS0), sdesc_sw128(a0 + kk * 32, 16, 1024),
@@ -178,6 +188,11 @@ __global__ void __launch_bounds__(320, 2)
       const uint32_t p0 = tmem + (q ? C::kColS1 : C::kColS0);
       mbar_wait(&p_full[q], par);
       tc_fence_after();
+      if constexpr (kD64K4) {
+        mma_ts_k4(tmem + (q ? C::kColO1 : C::kColO0), p0, sdesc_sw128(b0, C::kBN * 128, 1024), kIdescPV,
+                  accumulate ? 1u : 0u);
+        return;
+      }
 #pragma unroll
       for (int kk = 0; kk < C::kBN / 16; ++kk)
         mma_ts_elect(tmem + (q ? C::kColO1 : C::kColO0), p0 + kk * 8,

@@ -76,6 +76,11 @@ struct FwdCfgPair {
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 };
 
+#ifndef FMHA_PAIR_K4
+#define FMHA_PAIR_K4 0  // batched tcgen05 issue (four K-steps per elect.sync; measured neutral: off)
+#endif
+constexpr bool kPairK4 = FMHA_PAIR_K4 != 0;
+
 template <int D_, int kBN_, bool kBF16, int kEmuPer16 = 4>
 __global__ void __launch_bounds__(192, FwdCfgPair<D_, kBN_>::kCtasPerSm)
     fmha_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ,  // box 128 rows
@@ -207,6 +212,13 @@ __global__ void __launch_bounds__(192, FwdCfgPair<D_, kBN_>::kCtasPerSm)
       };
       auto mma_qk = [&](int buf, int kslot) {
         const uint32_t b0 = ring_addr + kslot * C::kSlotBytes;
+        if constexpr (kPairK4) {  // four K-steps per elect.sync, one batch per 64-column atom of d
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c)
+            mma_pair_ss_k4(tmem + C::col_s(buf), sdesc_sw128(sQ_addr + c * (C::kBM * 128), 16, 1024),
+                           sdesc_sw128(b0 + c * (C::kKRowsPerCta * 128), 16, 1024), kIdescQK, c > 0 ? 1u : 0u);
+          return;
+        }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off_a = (kk >> 2) * (C::kBM * 128) + (kk & 3) * 32;
@@ -217,6 +229,14 @@ __global__ void __launch_bounds__(192, FwdCfgPair<D_, kBN_>::kCtasPerSm)
       };
       auto mma_pv = [&](int buf, int vslot, bool accumulate) {
         const uint32_t b0 = ring_addr + vslot * C::kSlotBytes;
+        if constexpr (kPairK4) {
+#pragma unroll
+          for (int c = 0; c < C::kBN / 64; ++c)
+            mma_pair_ts_k4(tmem + C::kColO, tmem + C::col_s(buf) + c * 32,
+                           sdesc_sw128(b0 + c * 4 * 16 * 128, C::kBN * 128, 1024), kIdescPV,
+                           (accumulate || c > 0) ? 1u : 0u);
+          return;
+        }
 #pragma unroll
         for (int kk = 0; kk < C::kBN / 16; ++kk)
           mma_pair_ts_elect(tmem + C::kColO, tmem + C::col_s(buf) + kk * 8,
