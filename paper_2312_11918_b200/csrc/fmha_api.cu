@@ -461,6 +461,7 @@ struct Tuning {
   int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N)
   int dbs;                // d = 128 below pair128_min_n: double-buffered-S kernel (FMHA_TUNE_DBS)
   int emu64d;             // exp2 split of the two-CTA d = 64 kernel (FMHA_TUNE_EMU64D)
+  int64_t d64_min_n;      // d = 64 runs on the two-CTA kernel from this N (FMHA_TUNE_D64_N)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -470,7 +471,8 @@ const Tuning& tuning() {
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
                   env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
-                  env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4)};
+                  env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4),
+                  env("FMHA_TUNE_D64_N", 1024)};
   }();
   return t;
 }
@@ -483,16 +485,23 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kP
 //    double-buffered S, two CTAs per SM (+2 % at N = 8192, +3.5 % at 16384,
 //    +6 % on c5; -1 % at 4096 and -5..-10 % below, where the persistent
 //    ping-pong kernel's unit loop beats the per-CTA prologue / epilogue);
-//  * d = 64, N >= 1024: the two-CTA-per-SM ping-pong with 64-row K/V steps
-//    (+4 % at N = 1024 .. +6.8 % at 8192; equal at 512, slower on small
-//    ragged problems);
+//  * d = 64, N >= 1024 or enough heads to fill every SM: the two-CTA-per-SM
+//    ping-pong with 64-row K/V steps (+4 % at N = 1024 .. +6.8 % at 8192;
+//    +1..9 % at N = 128..1000 with 192+ heads; slower on few-head problems);
 //  * d = 256, N > 128: CTA pairs (M = 256 MMAs, each SM streams half of every
 //    K/V tile; a single Q tile would pay a whole padding CTA);
 //  * otherwise the persistent ping-pong kernel (d <= 128) or the single-CTA
 //    d = 256 kernel.
 Kernel select_kernel(const fmha_fwd_params* p) {
   const Tuning& t = tuning();
-  if (p->d == 64) return t.d64_ok && p->N >= 1024 ? Kernel::kD64TwoCta : Kernel::kPingPong64;
+  if (p->d == 64) {
+    // the two-CTA kernel from N = 1024, and below that whenever the ping-pong
+    // kernel's 256-row units would fill every SM (measured crossover: many heads
+    // win 1-9 % on two CTAs per SM, few-head problems lose 5-10 %)
+    const int64_t pp_units = p->L * p->h * ((p->N + 255) / 256);
+    const bool many = t.d64_min_n == 1024 && pp_units >= num_sms();
+    return t.d64_ok && (p->N >= t.d64_min_n || many) ? Kernel::kD64TwoCta : Kernel::kPingPong64;
+  }
   if (p->d == 128)
     return t.pair_ok && p->N >= t.pair128_min_n ? Kernel::kPair128 : t.dbs ? Kernel::kDbs128 : Kernel::kPingPong128;
   return t.pair_ok && p->N > 128 ? Kernel::kPair256 : Kernel::kSingle256;

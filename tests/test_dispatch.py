@@ -7,7 +7,9 @@ import paper_2312_11918_b200 as fm
 
 @pytest.mark.parametrize("shape,kernel", [
     ((1, 512, 1, 64), "fmha_fwd_sm100_kernel<64>"),       # c1
-    ((16, 512, 12, 64), "fmha_fwd_sm100_kernel<64>"),     # c2
+    ((16, 512, 12, 64), "fmha_fwd_d64_kernel"),           # c2: 384 ping-pong units fill every SM
+    ((1, 512, 16, 64), "fmha_fwd_sm100_kernel<64>"),      # few heads, short N
+    ((4, 768, 4, 64), "fmha_fwd_sm100_kernel<64>"),
     ((4, 1024, 32, 64), "fmha_fwd_d64_kernel"),           # d=64 from N = 1024
     ((4, 4096, 32, 64), "fmha_fwd_d64_kernel"),           # Table-1 d=64
     ((4, 4096, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # c3

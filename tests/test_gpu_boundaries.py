@@ -13,6 +13,8 @@ SHAPES = [  # (L, N, h, d)
     (1, 8191, 1, 128), (1, 8192, 1, 128), (1, 8193, 1, 128),     # ping-pong <-> CTA-pair d=128
     (2, 128, 3, 256), (2, 129, 3, 256), (1, 255, 2, 256), (1, 257, 2, 256),  # single CTA <-> pair d=256
     (3, 640, 5, 128), (4, 96, 7, 64),
+    # d=64 below N = 1024: two CTAs per SM once the ping-pong units would fill every SM
+    (16, 200, 12, 64), (64, 77, 12, 64), (148, 128, 1, 64), (147, 256, 1, 64), (2, 512, 74, 64),
 ]
 
 
@@ -35,7 +37,9 @@ def test_kernel_family_boundaries(shape, dt):
     o, lse = fm.fmha_fwd(q, k, v)
     torch.cuda.synchronize()
     assert fm.launch_count() == 1
-    assert fm.kernel_for(L, N, h, d, dt)
+    name = fm.kernel_for(L, N, h, d, dt)
+    if d == 64 and N < 1024:  # the unit-count rule (tests/test_dispatch.py)
+        assert name.startswith("fmha_fwd_d64_kernel") == (L * h * ((N + 255) // 256) >= 148), name
     qf, kf, vf = (x.float().permute(0, 2, 1, 3) for x in (q, k, v))  # (L, h, N, d)
     s = qf @ kf.transpose(-1, -2) / math.sqrt(d)
     lse_ref = torch.logsumexp(s, dim=-1)                               # (L, h, N)

@@ -9,6 +9,7 @@ only_d128 = len(sys.argv) > 1 and sys.argv[1] == "d128"  # (with FMHA_TUNE_DBS=1
 cases = [(1, 77, 2, 128, torch.float16), (2, 333, 3, 128, torch.bfloat16), (3, 130, 1, 128, torch.float16),
          (1, 1000, 150, 128, torch.float16)] if only_d128 else [(1, 200, 2, 64, torch.float16), (2, 333, 3, 128, torch.bfloat16), (1, 1000, 2, 256, torch.float16), (3, 130, 1, 128, torch.float16), (1, 1, 1, 64, torch.float16),
                          (1, 1100, 2, 64, torch.float16),      # d=64 two-CTA-per-SM kernel
+                         (16, 200, 12, 64, torch.bfloat16),    # the same below N = 1024 (many heads)
                          (1, 384, 2, 256, torch.bfloat16),     # CTA pair with a padding tile
                          (1, 8320, 1, 128, torch.bfloat16)]    # d=128 CTA-pair kernel
 for (L, N, h, d, dt) in cases:
