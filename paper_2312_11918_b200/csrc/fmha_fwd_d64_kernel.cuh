@@ -62,6 +62,10 @@ struct FwdCfgD64 {
 #define FMHA_D64_K4 1  // batched tcgen05 issue (four K-steps per elect.sync): +1.5 % on Table-1 d=64
 #endif
 constexpr bool kD64K4 = FMHA_D64_K4 != 0;
+#ifndef FMHA_D64_FUSED
+#define FMHA_D64_FUSED 0  // PV + S + commit of a tile step in one elect.sync block
+#endif
+constexpr bool kD64Fused = FMHA_D64_FUSED != 0;
 
 template <bool kBF16, int kEmuPer16 = 4>
 __global__ void __launch_bounds__(320, 2)
@@ -225,13 +229,27 @@ __global__ void __launch_bounds__(320, 2)
         // polling both barriers, is 3 % slower)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          mma_pv(q, vs, j > 1, par);
-          mma_qk(q, ks);
-          mma_commit_elect(&s_full[q]);
+          if constexpr (kD64Fused) {  // PV, S and the s_full commit in one issue block
+            mbar_wait(&p_full[q], par);
+            tc_fence_after();
+            mma_pv_qk_commit_k4(tmem + (q ? C::kColO1 : C::kColO0), tmem + (q ? C::kColS1 : C::kColS0),
+                                sdesc_sw128(ring_addr + vs * C::kKVTileBytes, C::kBN * 128, 1024), kIdescPV,
+                                j > 1 ? 1u : 0u, tmem + (q ? C::kColS1 : C::kColS0),
+                                sdesc_sw128(sQ_addr + q * C::kQTileBytes, 16, 1024),
+                                sdesc_sw128(ring_addr + ks * C::kKVTileBytes, 16, 1024), kIdescQK, &s_full[q]);
+          } else {
+            mma_pv(q, vs, j > 1, par);
+            mma_qk(q, ks);
+            mma_commit_elect(&s_full[q]);
+          }
         }
         if (j == n_kv - 1) mma_commit_elect(q_empty);  // last reads of Q issued
-        mma_commit_elect(&kv_empty[vs]);
-        mma_commit_elect(&kv_empty[ks]);
+        if constexpr (kD64Fused) {
+          mma_commit2_elect(&kv_empty[vs], &kv_empty[ks]);
+        } else {
+          mma_commit_elect(&kv_empty[vs]);
+          mma_commit_elect(&kv_empty[ks]);
+        }
         ++it;
       }
       const int vs = next_slot();

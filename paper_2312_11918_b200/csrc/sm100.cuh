@@ -408,6 +408,49 @@ __device__ __forceinline__ void mma_ts_k4_1t(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
+// One elect.sync for a whole d = 64 tile step: O += P V (four TS K-steps,
+// A = P in TMEM, B = V MN-major), S = Q K^T (four SS K-steps into s_tmem), then
+// tcgen05.commit to `bar` -- the two GEMMs and the commit of the two-CTA d = 64
+// kernel's inner loop in a single issue block.
+__device__ __forceinline__ void mma_pv_qk_commit_k4(uint32_t o_tmem, uint32_t p_tmem, uint64_t vdesc,
+                                                    uint32_t idesc_pv, uint32_t acc_pv, uint32_t s_tmem,
+                                                    uint64_t qdesc, uint64_t kdesc, uint32_t idesc_qk,
+                                                    uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t, z;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3, q1, q2, q3, k1, k2, k3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "setp.ne.b32 z, %4, %4;\n\t"
+      "add.s32 a1, %1, 8;\n\tadd.s32 a2, %1, 16;\n\tadd.s32 a3, %1, 24;\n\t"
+      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+      "add.s64 q1, %6, 2;\n\tadd.s64 q2, %6, 4;\n\tadd.s64 q3, %6, 6;\n\t"
+      "add.s64 k1, %7, 2;\n\tadd.s64 k2, %7, 4;\n\tadd.s64 k3, %7, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%5], %6, %7, %8, z;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%5], q1, k1, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%5], q2, k2, %8, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%5], q3, k3, %8, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n}\n" ::"r"(o_tmem),
+      "r"(p_tmem), "l"(vdesc), "r"(idesc_pv), "r"(acc_pv), "r"(s_tmem), "l"(qdesc), "l"(kdesc),
+      "r"(idesc_qk), "r"(smem_u32(bar))
+      : "memory");
+}
+// Two commits from one elect.sync.
+__device__ __forceinline__ void mma_commit2_elect(uint64_t* bar0, uint64_t* bar1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n}\n" ::"r"(
+          smem_u32(bar0)),
+      "r"(smem_u32(bar1))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
