@@ -462,6 +462,7 @@ struct Tuning {
   int dbs;                // d = 128 below pair128_min_n: double-buffered-S kernel (FMHA_TUNE_DBS)
   int emu64d;             // exp2 split of the two-CTA d = 64 kernel (FMHA_TUNE_EMU64D)
   int64_t d64_min_n;      // d = 64 runs on the two-CTA kernel from this N (FMHA_TUNE_D64_N)
+  int64_t tiny_tiles;     // at most this many Q tiles: one CTA per tile (FMHA_TUNE_TINY)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -472,12 +473,12 @@ const Tuning& tuning() {
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
                   env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
                   env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4),
-                  env("FMHA_TUNE_D64_N", 1024)};
+                  env("FMHA_TUNE_D64_N", 1024), env("FMHA_TUNE_TINY", -1)};
   }();
   return t;
 }
 
-enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kPair256, kSingle256 };
+enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kPair256, kSingle256, kSingleSmall };
 
 // Which kernel runs a (valid) problem; thresholds are measured crossovers
 // (profiles/r01_microbench.txt):
@@ -490,10 +491,31 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kP
 //    +1..9 % at N = 128..1000 with 192+ heads; slower on few-head problems);
 //  * d = 256, N > 128: CTA pairs (M = 256 MMAs, each SM streams half of every
 //    K/V tile; a single Q tile would pay a whole padding CTA);
+//  * d <= 128 with at most #SMs Q tiles of 128 rows: the single-CTA kernel
+//    (one CTA per Q tile, double-buffered S; +20..55 % on one-wave problems);
 //  * otherwise the persistent ping-pong kernel (d <= 128) or the single-CTA
 //    d = 256 kernel.
+// The host pipeline runs chunks / row slices of one problem: they must use the
+// kernel of the WHOLE problem, so its output is bitwise equal to one device
+// launch (tests/test_gpu_parity.py); set for the duration of the pipeline.
+thread_local int g_forced_kernel = -1;
+struct ForceKernel {
+  explicit ForceKernel(int k) { g_forced_kernel = k; }
+  ~ForceKernel() { g_forced_kernel = -1; }
+};
+
 Kernel select_kernel(const fmha_fwd_params* p) {
+  if (g_forced_kernel >= 0) return static_cast<Kernel>(g_forced_kernel);
   const Tuning& t = tuning();
+  // Problems of at most one wave of 128-row Q tiles (<= #SMs): one CTA per Q
+  // tile with double-buffered S.  The persistent kernels would put two tiles
+  // on each of only tiles/2 SMs (measured +20..55 %, tools/exp/tiny2.py).
+  // FMHA_TUNE_TINY overrides the tile limit (0: off).
+  {
+    const int64_t tiles = p->L * p->h * ((p->N + 127) / 128);
+    const int64_t limit = t.tiny_tiles >= 0 ? t.tiny_tiles : num_sms();
+    if (p->d <= 128 && tiles <= limit && !t.dbs && !t.split) return Kernel::kSingleSmall;
+  }
   if (p->d == 64) {
     // the two-CTA kernel from N = 1024, and below that whenever the ping-pong
     // kernel's 256-row units would fill every SM (measured crossover: many heads
@@ -516,6 +538,7 @@ const char* kernel_name(Kernel k) {
     case Kernel::kPair128: return "fmha_fwd_pair_kernel<128,64> (CTA pairs, two CTAs per SM)";
     case Kernel::kPair256: return "fmha_fwd_pair_kernel<256,128> (CTA pairs)";
     case Kernel::kSingle256: return "fmha_fwd_st_kernel<256,128> (single CTA)";
+    case Kernel::kSingleSmall: return "fmha_fwd_st_kernel<64|128,128> (one CTA per Q tile, tiny problems)";
   }
   return "";
 }
@@ -684,6 +707,12 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
       return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, mo, o, lse, st, nq)
                 : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, mo, o, lse, st, nq);
     }
+    case Kernel::kSingleSmall:
+      if (p->d == 64)
+        return bf ? launch_st<64, true, 128>(p, mq, mk, mv, mo, o, lse, st, nq)
+                  : launch_st<64, false, 128>(p, mq, mk, mv, mo, o, lse, st, nq);
+      return bf ? launch_st<128, true, 128>(p, mq, mk, mv, mo, o, lse, st, nq)
+                : launch_st<128, false, 128>(p, mq, mk, mv, mo, o, lse, st, nq);
     case Kernel::kSingle256:
     default:
       return bf ? launch_st<256, true, 128>(p, mq, mk, mv, mo, o, lse, st, nq)
@@ -715,6 +744,8 @@ fmha_status fmha_b200::fwd_host_pipeline(const fmha_fwd_params* p, const void* q
   fmha_status s = fmha_fwd_check(p);
   if (s != FMHA_OK) return s;
   if (!q || !k || !v || !o) return fail(FMHA_ERR_CONFIG, "null tensor pointer");
+  // every chunk / row slice runs the whole problem's kernel (bitwise equal to one launch)
+  ForceKernel force(static_cast<int>(select_kernel(p)));
   // Host buffers are BSHD views of the strides given; the device copies use
   // the same layout, so each region must be batch-major and non-overlapping
   // (the chunked copies move whole batches / row ranges of it).

@@ -6,15 +6,18 @@ import paper_2312_11918_b200 as fm
 
 
 @pytest.mark.parametrize("shape,kernel", [
-    ((1, 512, 1, 64), "fmha_fwd_sm100_kernel<64>"),       # c1
+    ((1, 512, 1, 64), "fmha_fwd_st_kernel<64|128"),       # c1: 4 Q tiles, one CTA each
+    ((1, 4096, 4, 128), "fmha_fwd_st_kernel<64|128"),     # 128 Q tiles <= 148 SMs
+    ((1, 512, 37, 64), "fmha_fwd_st_kernel<64|128"),      # 148 Q tiles
+    ((1, 512, 38, 64), "fmha_fwd_sm100_kernel<64>"),      # 152 Q tiles, few heads, short N
     ((16, 512, 12, 64), "fmha_fwd_d64_kernel"),           # c2: 384 ping-pong units fill every SM
-    ((1, 512, 16, 64), "fmha_fwd_sm100_kernel<64>"),      # few heads, short N
-    ((4, 768, 4, 64), "fmha_fwd_sm100_kernel<64>"),
+    ((1, 768, 40, 64), "fmha_fwd_sm100_kernel<64>"),
     ((4, 1024, 32, 64), "fmha_fwd_d64_kernel"),           # d=64 from N = 1024
+    ((2, 1024, 10, 64), "fmha_fwd_d64_kernel"),
     ((4, 4096, 32, 64), "fmha_fwd_d64_kernel"),           # Table-1 d=64
     ((4, 4096, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # c3
-    ((1, 8191, 2, 128), "fmha_fwd_sm100_kernel<128>"),
-    ((1, 8192, 2, 128), "fmha_fwd_pair_kernel<128,64>"),
+    ((3, 8191, 1, 128), "fmha_fwd_sm100_kernel<128>"),
+    ((3, 8192, 1, 128), "fmha_fwd_pair_kernel<128,64>"),
     ((8, 16384, 32, 128), "fmha_fwd_pair_kernel<128,64>"),  # c5
     ((2, 8192, 8, 256), "fmha_fwd_pair_kernel<256,128>"),  # c4
     ((1, 129, 2, 256), "fmha_fwd_pair_kernel<256,128>"),   # two Q tiles (one padded)

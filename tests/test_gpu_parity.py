@@ -53,8 +53,18 @@ def test_small_full(oracle, d, dt):
 @pytest.mark.parametrize("N", [1024, 2048])
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
 def test_d64_two_ctas_per_sm_full(oracle, N, dt):
-    """d = 64, N >= 1024 runs the two-CTA-per-SM kernel (64-row K/V steps)."""
-    _full_check(oracle, 1, N, 3, 64, dt, seed=13)
+    """d = 64, N >= 1024 (more Q tiles than SMs) runs the two-CTA-per-SM kernel (64-row K/V steps)."""
+    import paper_2312_11918_b200 as fm
+    assert fm.kernel_for(1, N, 20, 64).startswith("fmha_fwd_d64_kernel")
+    _full_check(oracle, 1, N, 20, 64, dt, seed=13)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_persistent_ping_pong_full(oracle, d):
+    """More Q tiles than SMs, few heads, N < 1024: the persistent two-Q-tile ping-pong."""
+    import paper_2312_11918_b200 as fm
+    assert fm.kernel_for(1, 640, 32, d).startswith("fmha_fwd_sm100_kernel")
+    _full_check(oracle, 1, 640, 32, d, "f16", seed=17)
 
 
 def test_config2_distilbert_full(oracle):
