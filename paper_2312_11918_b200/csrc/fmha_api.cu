@@ -463,6 +463,7 @@ struct Tuning {
   int emu64d;             // exp2 split of the two-CTA d = 64 kernel (FMHA_TUNE_EMU64D)
   int64_t d64_min_n;      // d = 64 runs on the two-CTA kernel from this N (FMHA_TUNE_D64_N)
   int64_t tiny_tiles;     // at most this many Q tiles: one CTA per tile (FMHA_TUNE_TINY)
+  int64_t tiny2_tiles;    // up to this many Q tiles: one CTA per tile, two per SM (FMHA_TUNE_TINY2)
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -473,12 +474,14 @@ const Tuning& tuning() {
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
                   env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
                   env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4),
-                  env("FMHA_TUNE_D64_N", 1024), env("FMHA_TUNE_TINY", -1)};
+                  env("FMHA_TUNE_D64_N", 1024), env("FMHA_TUNE_TINY", -1),
+                  env("FMHA_TUNE_TINY2", -1)};
   }();
   return t;
 }
 
-enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kPair256, kSingle256, kSingleSmall };
+enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kPair256, kSingle256, kSingleSmall,
+                    kSingleSmall2 };
 
 // Which kernel runs a (valid) problem; thresholds are measured crossovers
 // (profiles/r01_microbench.txt):
@@ -493,6 +496,8 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kP
 //    K/V tile; a single Q tile would pay a whole padding CTA);
 //  * d <= 128 with at most #SMs Q tiles of 128 rows: the single-CTA kernel
 //    (one CTA per Q tile, double-buffered S; +20..55 % on one-wave problems);
+//    up to 2 x #SMs tiles (d = 128: N <= 2048) its 64-row-K/V-step form, two
+//    CTAs per SM (+0..19 %);
 //  * otherwise the persistent ping-pong kernel (d <= 128) or the single-CTA
 //    d = 256 kernel.
 // The host pipeline runs chunks / row slices of one problem: they must use the
@@ -515,6 +520,10 @@ Kernel select_kernel(const fmha_fwd_params* p) {
     const int64_t tiles = p->L * p->h * ((p->N + 127) / 128);
     const int64_t limit = t.tiny_tiles >= 0 ? t.tiny_tiles : num_sms();
     if (p->d <= 128 && tiles <= limit && !t.dbs && !t.split) return Kernel::kSingleSmall;
+    // up to two waves: one CTA per tile with 64-row K/V steps, two CTAs per SM
+    // (d = 64: +0..19 %; d = 128: +4..12 % up to N = 2048, -3 % at N = 4096)
+    const int64_t limit2 = t.tiny2_tiles >= 0 ? t.tiny2_tiles : (p->d == 64 || p->N <= 2048 ? 2 * num_sms() : 0);
+    if (p->d <= 128 && tiles <= limit2 && !t.dbs && !t.split) return Kernel::kSingleSmall2;
   }
   if (p->d == 64) {
     // the two-CTA kernel from N = 1024, and below that whenever the ping-pong
@@ -539,6 +548,7 @@ const char* kernel_name(Kernel k) {
     case Kernel::kPair256: return "fmha_fwd_pair_kernel<256,128> (CTA pairs)";
     case Kernel::kSingle256: return "fmha_fwd_st_kernel<256,128> (single CTA)";
     case Kernel::kSingleSmall: return "fmha_fwd_st_kernel<64|128,128> (one CTA per Q tile, tiny problems)";
+    case Kernel::kSingleSmall2: return "fmha_fwd_st_kernel<64|128,64> (one CTA per Q tile, two CTAs per SM)";
   }
   return "";
 }
@@ -706,6 +716,16 @@ static fmha_status fwd_rows(const fmha_fwd_params* p, const void* q, const void*
         return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (K, 64-row boxes)");
       return bf ? launch_pair<256, 128, true, 4>(p, mq, mk64, mv, mo, o, lse, st, nq)
                 : launch_pair<256, 128, false, 4>(p, mq, mk64, mv, mo, o, lse, st, nq);
+    }
+    case Kernel::kSingleSmall2: {  // 64-row K/V steps: 256 TMEM columns, two CTAs per SM
+      CUtensorMap mk64, mv64;
+      if (!make_map(&mk64, k, p->dtype, p, p->k_stride, 64) || !make_map(&mv64, v, p->dtype, p, p->v_stride, 64))
+        return fail(FMHA_ERR_CUDA, "cuTensorMapEncodeTiled failed (64-row K/V maps)");
+      if (p->d == 64)
+        return bf ? launch_st<64, true, 64>(p, mq, mk64, mv64, mo, o, lse, st, nq)
+                  : launch_st<64, false, 64>(p, mq, mk64, mv64, mo, o, lse, st, nq);
+      return bf ? launch_st<128, true, 64>(p, mq, mk64, mv64, mo, o, lse, st, nq)
+                : launch_st<128, false, 64>(p, mq, mk64, mv64, mo, o, lse, st, nq);
     }
     case Kernel::kSingleSmall:
       if (p->d == 64)

@@ -6,15 +6,17 @@ import paper_2312_11918_b200 as fm
 
 
 @pytest.mark.parametrize("shape,kernel", [
-    ((1, 512, 1, 64), "fmha_fwd_st_kernel<64|128"),       # c1: 4 Q tiles, one CTA each
-    ((1, 4096, 4, 128), "fmha_fwd_st_kernel<64|128"),     # 128 Q tiles <= 148 SMs
-    ((1, 512, 37, 64), "fmha_fwd_st_kernel<64|128"),      # 148 Q tiles
-    ((1, 512, 38, 64), "fmha_fwd_sm100_kernel<64>"),      # 152 Q tiles, few heads, short N
-    ((16, 512, 12, 64), "fmha_fwd_d64_kernel"),           # c2: 384 ping-pong units fill every SM
-    ((1, 768, 40, 64), "fmha_fwd_sm100_kernel<64>"),
-    ((4, 1024, 32, 64), "fmha_fwd_d64_kernel"),           # d=64 from N = 1024
-    ((2, 1024, 10, 64), "fmha_fwd_d64_kernel"),
+    ((1, 512, 1, 64), "fmha_fwd_st_kernel<64|128,128>"),  # c1: 4 Q tiles, one CTA each
+    ((1, 4096, 4, 128), "fmha_fwd_st_kernel<64|128,128>"),  # 128 Q tiles <= 148 SMs
+    ((1, 512, 37, 64), "fmha_fwd_st_kernel<64|128,128>"),  # 148 Q tiles
+    ((1, 512, 38, 64), "fmha_fwd_st_kernel<64|128,64>"),   # 152 Q tiles: one CTA per tile, two per SM
+    ((1, 1024, 37, 64), "fmha_fwd_st_kernel<64|128,64>"),  # 296 Q tiles
+    ((1, 1024, 38, 64), "fmha_fwd_d64_kernel"),           # 304 Q tiles, N >= 1024
+    ((1, 512, 75, 64), "fmha_fwd_d64_kernel"),            # 300 Q tiles, 150 ping-pong units
+    ((16, 512, 12, 64), "fmha_fwd_d64_kernel"),           # c2: 768 Q tiles
     ((4, 4096, 32, 64), "fmha_fwd_d64_kernel"),           # Table-1 d=64
+    ((1, 2048, 18, 128), "fmha_fwd_st_kernel<64|128,64>"),  # 288 Q tiles, N <= 2048
+    ((1, 4096, 8, 128), "fmha_fwd_sm100_kernel<128>"),    # 256 Q tiles but N > 2048
     ((4, 4096, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # c3
     ((3, 8191, 1, 128), "fmha_fwd_sm100_kernel<128>"),
     ((3, 8192, 1, 128), "fmha_fwd_pair_kernel<128,64>"),

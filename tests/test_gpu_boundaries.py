@@ -9,11 +9,11 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 SHAPES = [  # (L, N, h, d)
-    (10, 1023, 2, 64), (10, 1024, 2, 64), (2, 1025, 3, 64),      # ping-pong <-> two-CTA d=64
+    (1, 1024, 37, 64), (1, 1024, 38, 64), (2, 1025, 3, 64),      # one CTA per tile <-> two-CTA d=64
     (3, 8191, 1, 128), (3, 8192, 1, 128), (3, 8193, 1, 128),     # ping-pong <-> CTA-pair d=128
     (1, 512, 37, 64), (1, 512, 38, 64), (1, 4096, 4, 128),       # one CTA per Q tile up to #SMs tiles
-    (1, 1000, 20, 64), (1, 1000, 20, 128), (2, 1100, 10, 64),    # ragged N on the persistent kernels
-    (2, 333, 40, 64),
+    (1, 1000, 40, 64), (3, 2100, 4, 128), (2, 1100, 20, 64),     # ragged N on the persistent kernels
+    (2, 333, 40, 64), (1, 512, 38, 64), (2, 700, 21, 128), (1, 300, 99, 64),
     (2, 128, 3, 256), (2, 129, 3, 256), (1, 255, 2, 256), (1, 257, 2, 256),  # single CTA <-> pair d=256
     (3, 640, 5, 128), (4, 96, 7, 64),
     # d=64 below N = 1024: two CTAs per SM once the ping-pong units would fill every SM
@@ -43,7 +43,7 @@ def test_kernel_family_boundaries(shape, dt):
     assert fm.launch_count() == 1
     name = fm.kernel_for(L, N, h, d, dt)
     tiles = L * h * ((N + 127) // 128)
-    if d <= 128 and tiles <= 148:  # one wave of Q tiles: one CTA per tile (tests/test_dispatch.py)
+    if d <= 128 and (tiles <= 148 or (tiles <= 296 and (d == 64 or N <= 2048))):  # one CTA per tile
         assert name.startswith("fmha_fwd_st_kernel"), name
     elif d == 64 and N < 1024:  # the unit-count rule
         assert name.startswith("fmha_fwd_d64_kernel") == (L * h * ((N + 255) // 256) >= 148), name
