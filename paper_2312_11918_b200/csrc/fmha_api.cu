@@ -524,6 +524,17 @@ Kernel select_kernel(const fmha_fwd_params* p) {
     // (d = 64: +0..19 %; d = 128: +4..12 % up to N = 2048, -3 % at N = 4096)
     const int64_t limit2 = t.tiny2_tiles >= 0 ? t.tiny2_tiles : (p->d == 64 || p->N <= 2048 ? 2 * num_sms() : 0);
     if (p->d <= 128 && tiles <= limit2 && !t.dbs && !t.split) return Kernel::kSingleSmall2;
+    // d = 128, 1536 <= N <= 4096: when the persistent kernel runs several rounds
+    // of 256-row units and leaves its last one mostly empty (units / #SMs just
+    // above an integer),
+    // the non-persistent form rebalances tile by tile: +5..8 % at wave
+    // efficiency 0.87 (L=2,h=16,N=4096; L=8,h=16,N=1536; L=4,h=16,N=3072), while
+    // well-quantised problems (c3: 1024 units, 0.99) stay persistent (+5 %).
+    if (p->d == 128 && p->N >= 1536 && p->N <= 4096 && t.tiny2_tiles < 0 && !t.dbs && !t.split) {
+      const int64_t units = p->L * p->h * ((p->N + 255) / 256), sms = num_sms();
+      const double eff = static_cast<double>(units) / static_cast<double>(((units + sms - 1) / sms) * sms);
+      if (units > sms && eff < 0.9) return Kernel::kSingleSmall2;
+    }
   }
   if (p->d == 64) {
     // the two-CTA kernel from N = 1024, and below that whenever the ping-pong
