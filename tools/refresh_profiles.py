@@ -29,7 +29,11 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def ncu_metrics(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    csv_path = rep.replace(".ncu-rep", "_raw.csv")
+    if not os.path.exists(rep) and os.path.exists(csv_path):  # exported on the GPU box (64 MiB pull limit)
+        raw = open(csv_path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     return rows[0], rows[1], rows[2]
 
@@ -46,7 +50,7 @@ def main(tag):
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
     for c in ("c2", "c3", "c4", "c5"):
         rep = os.path.join(OUT, f"prof_{c}.ncu-rep")
-        if not os.path.exists(rep):
+        if not os.path.exists(rep) and not os.path.exists(rep.replace(".ncu-rep", "_raw.csv")):
             continue
         h, u, v = ncu_metrics(rep)
         d = {n: (un, val) for n, un, val in zip(h, u, v)}
