@@ -11,11 +11,16 @@ import paper_2312_11918_b200 as fm
 
 random.seed(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 n_cases = int(sys.argv[2]) if len(sys.argv) > 2 else 150
+wide = len(sys.argv) > 3 and sys.argv[3] == "wide"  # many heads: the one-/two-CTA-per-tile and wave-quantised paths
 worst = {}
 for case in range(n_cases):
     d = random.choice([64, 128, 256])
-    N = random.choice([random.randint(1, 300), random.randint(300, 2100), random.randint(7000, 9000)])
-    L, h = random.randint(1, 3), random.randint(1, 5)
+    if wide:
+        N = random.choice([random.randint(1, 600), random.randint(600, 4200)])
+        L, h = random.randint(1, 4), random.randint(6, 48)
+    else:
+        N = random.choice([random.randint(1, 300), random.randint(300, 2100), random.randint(7000, 9000)])
+        L, h = random.randint(1, 3), random.randint(1, 5)
     dt = random.choice([torch.float16, torch.bfloat16])
     g = torch.Generator(device="cuda").manual_seed(case)
     scale_in = random.choice([0.5, 1.0, 3.0])
