@@ -183,6 +183,14 @@ constexpr bool kSeq = FMHA_SEQ != 0;
 #define FMHA_SPEC 0
 #endif
 constexpr bool kSpec = FMHA_SPEC != 0;  // speculative first half (see the softmax loop)
+// FMHA_PP_MASKED_MUFU=0: the padded last K/V tile takes the same exp2 code as
+// every other tile (polynomial lanes give 2^-125 instead of 0 for masked
+// scores; padded V rows are TMA zero-fill, so O is unchanged) -- one copy of
+// the unrolled exponential loop instead of two, a smaller hot loop body.
+#ifndef FMHA_PP_MASKED_MUFU
+#define FMHA_PP_MASKED_MUFU 1
+#endif
+constexpr bool kMaskedMufu = FMHA_PP_MASKED_MUFU != 0;
 #ifndef FMHA_PP_SOFTMAX_SLEEP_NS
 #define FMHA_PP_SOFTMAX_SLEEP_NS 0  // softmax wait for S: nanosleep between polls (0: try_wait loop)
 #endif
@@ -248,6 +256,11 @@ __device__ __forceinline__ void stage_o_tile(uint32_t tO, uint8_t* stage, int r,
 }
 
 // unit -> (b, head, q-block)
+template <bool B>
+struct BoolTag {
+  static constexpr bool value = B;
+};
+
 __device__ __forceinline__ void decode_unit(int u, int n_qb, int H, int& b, int& head, int& qb) {
   qb = u % n_qb;
   const int t = u / n_qb;
@@ -288,6 +301,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_kv = args.n_kv_tiles;
+  const int n_full = (args.N % C::kBN) ? n_kv - 1 : n_kv;  // K/V steps without padding columns
 #ifdef FMHA_TRACE_BUILD
   const bool tr = args.trace != nullptr && blockIdx.x == 0;
 #else
@@ -689,7 +703,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
       float m = -INFINITY;  // running max in raw score units
       float l = 0.0f;       // running sum of exp2((s - m) * sl2)
 
-      for (int j = 0; j < n_kv; ++j, ++it) {
+      // One K/V step of the softmax.  The padded last tile (N % 128 != 0) runs
+      // its own instantiation after the loop, so the hot loop body carries no
+      // masking code (a smaller unrolled body: fewer instruction-fetch stalls).
+      auto kv_step = [&](const int j, auto padded_tag) {
+        constexpr bool kPadded = decltype(padded_tag)::value;
         prof.mark(7);
 #ifdef FMHA_SPIN_S
         while (!mbar_test_wait(a_s_full, it & 1)) {
@@ -715,7 +733,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
           mbar_arrive_addr(a_p_full0);
           mbar_arrive_addr(a_p_full1);
           prof.mark(5);
-          continue;
+          return;
         }
 #endif
         uint32_t sr[128];
@@ -727,8 +745,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         float s[128];
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
-        const int valid = N - j * C::kBN;  // columns >= valid are padding
-        if (valid < C::kBN) {
+        if constexpr (kPadded) {
+          const int valid = N - j * C::kBN;  // columns >= valid are padding
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c >= valid) s[c] = -INFINITY;
@@ -774,7 +792,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         // tile, half 0 is exponentiated speculatively against the stale max
         // while the new row max is reduced in the same instruction stream;
         // only when a row's max grew by more than 8 is the half redone.
-        const bool masked = valid < C::kBN;
+        constexpr bool masked = kPadded;
         uint32_t p0[32], p1[32];
         // The exponential phases of the two WGs run in strict turns (named
         // barriers kSeqBar + q): each gets the sub-partitions' MUFU / FMA
@@ -818,14 +836,20 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         } else {
         if (redo) {
           neg = -m * sl2;
-          rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
-                      : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+          if constexpr (kMaskedMufu)
+            rs = masked ? exp_rowsum_pack<kBF16, 0, 64, 0>(s, sl2, neg, p0)
+                        : exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
+          else
+            rs = exp_rowsum_pack<kBF16, 0, 64, kEmuPer16>(s, sl2, neg, p0);
         }
         trace_stamp(args, trq, q, j, 9);
         prof.mark(3);
         tmem_st32x32b_x32(tS, p0);
-        rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
-                     : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        if constexpr (kMaskedMufu)
+          rs += masked ? exp_rowsum_pack<kBF16, 64, 64, 0>(s, sl2, neg, p1)
+                       : exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
+        else
+          rs += exp_rowsum_pack<kBF16, 64, 64, kEmuPer16>(s, sl2, neg, p1);
         }
         if constexpr (kSeq) named_bar_arrive(C::kSeqBar + (q ^ 1), 256);
         prof.mark(4);
@@ -849,6 +873,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::kThreads, 1)
         // per-warp completion times of the first unit: trace[(2*n_kv + j)*16 + warp]
         if (tr && i == 0 && lane == 0) args.trace[(2 * n_kv + j) * 16 + warp] = clock64();
 #endif
+      };
+      for (int j = 0; j < n_full; ++j, ++it) kv_step(j, BoolTag<false>{});
+      if (n_full < n_kv) {
+        kv_step(n_kv - 1, BoolTag<true>{});
+        ++it;
       }
 
       if (C::kEpiWG && u + static_cast<int>(gridDim.x) < args.n_units) {

@@ -10,6 +10,9 @@
 //       polynomial with the MUFU stream instead of hoisting it
 //   V3  V2 + MUFU inputs of the next group depending on the polynomial
 //       result (strict alternation)
+//   V5  the ping-pong kernel's step verbatim: x128 load, row max + __any_sync
+//       rescale vote, two exp_rowsum_pack halves, P stores each followed by
+//       wait::st + fence + a per-thread mbarrier arrive (the p_full publish)
 //   V4  the d=128 pair kernel's 64-column tile (x64 load, 64 exps, one x32
 //       store), 1-4 warps per sub-partition (clk per 64-column tile)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -maxrregcount=168 \
@@ -65,7 +68,13 @@ __device__ __forceinline__ float exp_rowsum_pack_il(const float (&s)[128], float
 template <int V>
 __global__ void __launch_bounds__(V == 4 ? 512 : 256, 1) probe(int iters, float zero, long long* clk, float* sink) {
   __shared__ uint32_t tmem_holder;
+  __shared__ uint64_t pbar[2];
   const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&pbar[0], blockDim.x);
+    mbar_init(&pbar[1], blockDim.x);
+    fence_mbar_init();
+  }
   if (warp == 0) tmem_alloc(&tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
@@ -83,6 +92,8 @@ __global__ void __launch_bounds__(V == 4 ? 512 : 256, 1) probe(int iters, float 
   }
   const uint64_t zero2 = f2_pack(zero, zero);
   float l = 0.f;
+  float m_run = -INFINITY;
+  long long h0_clk = 0;
   __syncthreads();
   const long long c0 = clock64();
   for (int it = 0; it < iters; ++it) {
@@ -105,6 +116,46 @@ __global__ void __launch_bounds__(V == 4 ? 512 : 256, 1) probe(int iters, float 
       tmem_st32x32b_x32(base + 64, p0);
       tmem_wait_st();
       __syncwarp();
+      continue;
+    }
+    if constexpr (V == 5) {  // the ping-pong kernel's softmax step
+      uint32_t sr[128];
+      tmem_ld32x32b_x128(base, sr);
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sr[c]);
+      float mx[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mx[t] = fmaxf(s[t], s[t + 8]);
+#pragma unroll
+      for (int c = 16; c < 128; c += 16)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mx[t] = fmaxf(mx[t], fmaxf(s[c + t], s[c + t + 8]));
+      const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      const float sl2 = 0.1275f;
+      if (__any_sync(0xffffffffu, (mt - m_run) * sl2 > 8.0f)) {
+        const float mn = fmaxf(mt, m_run);
+        l *= ex2_approx((m_run - mn) * sl2);
+        m_run = mn;
+      }
+      const float neg = -m_run * sl2;
+      uint32_t p0[32], p1[32];
+      long long t0;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
+      float rs = exp_rowsum_pack<false, 0, 64, 4>(s, sl2, neg, p0);
+      long long t1;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
+      h0_clk += t1 - t0;
+      tmem_st32x32b_x32(base + 128, p0);
+      rs += exp_rowsum_pack<false, 64, 64, 4>(s, sl2, neg, p1);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&pbar[0]);
+      tmem_st32x32b_x32(base + 160, p1);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&pbar[1]);
+      l += rs;
       continue;
     }
     uint32_t sr[128];
@@ -145,6 +196,7 @@ __global__ void __launch_bounds__(V == 4 ? 512 : 256, 1) probe(int iters, float 
   }
   const long long c1 = clock64();
   if ((threadIdx.x & 31) == 0) clk[blockIdx.x * 16 + warp] = c1 - c0;
+  if (V == 5 && threadIdx.x == 0 && blockIdx.x == 0) printf("V5 exps half 0: %lld clk per tile (warp 0)\n", h0_clk / iters);
   sink[blockIdx.x * blockDim.x + threadIdx.x] = l;
   tc_fence_before();
   __syncthreads();
@@ -182,6 +234,7 @@ int main() {
     run<2>(t);
     run<3>(t);
     run<4>(t);
+    run<5>(t);
   }
   run<4>(384);  // three warps per SMSP
   run<4>(512);
