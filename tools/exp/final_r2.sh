@@ -10,6 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 for c in c3 c2 c4 c5; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:fmha_fwd -s 3 -c 1 -o gpurun_out/prof_$c python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-configs > /dev/null 2>&1
   # the pull back is capped at 64 MiB: keep c3's report, export the others' raw metrics
+  if [ $c = c3 ]; then ncu -i gpurun_out/prof_c3.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/prof_c3_source.csv.gz; fi
   if [ $c != c3 ]; then ncu -i gpurun_out/prof_$c.ncu-rep --page raw --csv > gpurun_out/prof_${c}_raw.csv 2>/dev/null && rm -f gpurun_out/prof_$c.ncu-rep; fi
 done
 python tools/exp/clock_under_load.py c3 c5 c4 c2 > gpurun_out/sustained.txt 2>&1; cat gpurun_out/sustained.txt
