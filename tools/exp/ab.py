@@ -13,7 +13,9 @@ extra = [(4, 16, 4096, 128, torch.bfloat16), (2, 16, 8192, 128, torch.float16), 
          (1, 16, 16384, 128, torch.float16), (8, 16, 2048, 128, torch.float16), (16, 16, 1024, 128, torch.float16),
          (16, 32, 1024, 64, torch.float16), (8, 32, 2048, 64, torch.float16), (2, 32, 8192, 64, torch.float16),
          (4, 32, 4096, 64, torch.bfloat16), (1, 1, 512, 64, torch.float16), (32, 16, 256, 64, torch.float16),
-         (16, 12, 768, 64, torch.float16), (4, 16, 4000, 128, torch.float16)]
+         (16, 12, 768, 64, torch.float16), (4, 16, 4000, 128, torch.float16),
+         (1, 20, 1024, 64, torch.bfloat16), (1, 32, 640, 128, torch.float16), (2, 8, 1024, 128, torch.float16),
+         (1, 8, 1000, 128, torch.float16)]
 shapes += extra
 if len(sys.argv) > 2:
     shapes = [shapes[int(i)] for i in sys.argv[2].split(",")]
