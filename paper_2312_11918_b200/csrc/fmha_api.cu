@@ -458,7 +458,7 @@ struct Tuning {
   bool pair_ok, d64_ok;
   int emu64, emu128;
   int split;  // split-row ping-pong for d <= 128 (FMHA_TUNE_SPLIT)
-  int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N)
+  int64_t pair128_min_n;  // d = 128 runs on CTA pairs from this N (FMHA_TUNE_PAIR128_N; default: never)
   int dbs;                // d = 128 below pair128_min_n: double-buffered-S kernel (FMHA_TUNE_DBS)
   int emu64d;             // exp2 split of the two-CTA d = 64 kernel (FMHA_TUNE_EMU64D)
   int64_t d64_min_n;      // d = 64 runs on the two-CTA kernel from this N (FMHA_TUNE_D64_N)
@@ -472,7 +472,7 @@ const Tuning& tuning() {
       return e ? std::atoi(e) : dflt;
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
-                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 8192),
+                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 1 << 30),
                   env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4),
                   env("FMHA_TUNE_D64_N", 1024), env("FMHA_TUNE_TINY", -1),
                   env("FMHA_TUNE_TINY2", -1)};
@@ -485,10 +485,12 @@ enum class Kernel { kPingPong64, kD64TwoCta, kPingPong128, kDbs128, kPair128, kP
 
 // Which kernel runs a (valid) problem; thresholds are measured crossovers
 // (profiles/r01_microbench.txt):
-//  * d = 128, N >= 8192: CTA pairs with one Q tile per CTA and 64-column
-//    double-buffered S, two CTAs per SM (+2 % at N = 8192, +3.5 % at 16384,
-//    +6 % on c5; -1 % at 4096 and -5..-10 % below, where the persistent
-//    ping-pong kernel's unit loop beats the per-CTA prologue / epilogue);
+//  * d = 128: the persistent ping-pong kernel at every N beyond the one-tile
+//    paths.  Since its padded-step split it beats the CTA-pair kernel at long
+//    sequences too (N = 8192 +4..8 %, N = 16384 +4 %, c5 +2 % at a lower
+//    power-capped clock); FMHA_TUNE_PAIR128_N=<N> keeps the pair kernel
+//    (one Q tile per CTA, 64-column double-buffered S, two CTAs per SM) as an
+//    opt-in from that N;
 //  * d = 64, N >= 1024 or enough heads to fill every SM: the two-CTA-per-SM
 //    ping-pong with 64-row K/V steps (+4 % at N = 1024 .. +6.8 % at 8192;
 //    +1..9 % at N = 128..1000 with 192+ heads; slower on few-head problems);
@@ -524,17 +526,10 @@ Kernel select_kernel(const fmha_fwd_params* p) {
     // (d = 64: +0..19 %; d = 128: +4..12 % up to N = 2048, -3 % at N = 4096)
     const int64_t limit2 = t.tiny2_tiles >= 0 ? t.tiny2_tiles : (p->d == 64 || p->N <= 2048 ? 2 * num_sms() : 0);
     if (p->d <= 128 && tiles <= limit2 && !t.dbs && !t.split) return Kernel::kSingleSmall2;
-    // d = 128, 1536 <= N <= 4096: when the persistent kernel runs several rounds
-    // of 256-row units and leaves its last one mostly empty (units / #SMs just
-    // above an integer),
-    // the non-persistent form rebalances tile by tile: +5..8 % at wave
-    // efficiency 0.87 (L=2,h=16,N=4096; L=8,h=16,N=1536; L=4,h=16,N=3072), while
-    // well-quantised problems (c3: 1024 units, 0.99) stay persistent (+5 %).
-    if (p->d == 128 && p->N >= 1536 && p->N <= 4096 && t.tiny2_tiles < 0 && !t.dbs && !t.split) {
-      const int64_t units = p->L * p->h * ((p->N + 255) / 256), sms = num_sms();
-      const double eff = static_cast<double>(units) / static_cast<double>(((units + sms - 1) / sms) * sms);
-      if (units > sms && eff < 0.9) return Kernel::kSingleSmall2;
-    }
+    // (A wave-quantisation rule that sent badly quantised d = 128 mid-N problems
+    // to this non-persistent form was +5..8 % before the ping-pong kernel's
+    // padded-step split and is 3..6 % slower since: removed,
+    // profiles/r02_microbench.txt.)
   }
   if (p->d == 64) {
     // the two-CTA kernel from N = 1024, and below that whenever the ping-pong

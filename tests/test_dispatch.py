@@ -18,12 +18,11 @@ import paper_2312_11918_b200 as fm
     ((1, 2048, 18, 128), "fmha_fwd_st_kernel<64|128,64>"),  # 288 Q tiles, N <= 2048
     ((1, 4096, 8, 128), "fmha_fwd_sm100_kernel<128>"),    # 256 Q tiles but N > 2048
     ((4, 4096, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # c3: 1024 units, wave efficiency 0.99
-    ((2, 4096, 16, 128), "fmha_fwd_st_kernel<64|128,64>"),  # 512 units, efficiency 0.86
+    ((2, 4096, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # 512 units (wave efficiency 0.86: still persistent)
     ((8, 2048, 16, 128), "fmha_fwd_sm100_kernel<128>"),   # 1024 units
-    ((16, 1024, 16, 128), "fmha_fwd_sm100_kernel<128>"),  # N < 1536
-    ((3, 8191, 1, 128), "fmha_fwd_sm100_kernel<128>"),
-    ((3, 8192, 1, 128), "fmha_fwd_pair_kernel<128,64>"),
-    ((8, 16384, 32, 128), "fmha_fwd_pair_kernel<128,64>"),  # c5
+    ((16, 1024, 16, 128), "fmha_fwd_sm100_kernel<128>"),
+    ((3, 8192, 1, 128), "fmha_fwd_sm100_kernel<128>"),    # long d=128: ping-pong (CTA pairs are opt-in)
+    ((8, 16384, 32, 128), "fmha_fwd_sm100_kernel<128>"),  # c5
     ((2, 8192, 8, 256), "fmha_fwd_pair_kernel<256,128>"),  # c4
     ((1, 129, 2, 256), "fmha_fwd_pair_kernel<256,128>"),   # two Q tiles (one padded)
     ((1, 128, 2, 256), "fmha_fwd_st_kernel<256,128>"),     # a single Q tile

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [  # (L, N, h, d)
     (1, 1024, 37, 64), (1, 1024, 38, 64), (2, 1025, 3, 64),      # one CTA per tile <-> two-CTA d=64
-    (3, 8191, 1, 128), (3, 8192, 1, 128), (3, 8193, 1, 128),     # ping-pong <-> CTA-pair d=128
+    (3, 8191, 1, 128), (3, 8192, 1, 128), (3, 8193, 1, 128),     # long d=128, ragged last tile
     (1, 512, 37, 64), (1, 512, 38, 64), (1, 4096, 4, 128),       # one CTA per Q tile up to #SMs tiles
     (1, 1000, 40, 64), (3, 2100, 4, 128), (2, 1100, 20, 64),     # ragged N on the persistent kernels
     (2, 333, 40, 64), (1, 512, 38, 64), (2, 700, 21, 128), (1, 300, 99, 64),

@@ -154,7 +154,7 @@ def test_strided_views(oracle, d, N):
 @pytest.mark.parametrize("cfg", [(4, 4096, 16, 128, "f16"), (2, 8192, 8, 256, "f16"),
                                  (8, 16384, 32, 128, "bf16"), (1, 8320, 2, 128, "f16"),
                                  (1, 2432, 3, 256, "bf16"), (4, 4096, 32, 64, "f16")],
-                         ids=["c3", "c4", "c5", "d128-pair-odd-tiles", "d256-pair-odd-tiles", "table1-d64"])
+                         ids=["c3", "c4", "c5", "d128-long-odd-tiles", "d256-pair-odd-tiles", "table1-d64"])
 def test_large_configs_sampled(oracle, cfg):
     """c3/c4/c5 at full size: inputs generated on the device (seeded torch
     RNG, rounded to the 16-bit type), every (b, head) computed on the GPU,
@@ -301,6 +301,47 @@ def test_pair_kernel_matches_single_cta_kernel_bitwise(oracle, tmp_path):
     ref = np.load(tmp_path / "out.npz")
     np.testing.assert_array_equal(o.float().cpu().numpy(), ref["o"])
     np.testing.assert_array_equal(lse.cpu().numpy(), ref["lse"])
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_opt_in_d128_pair_kernel_against_oracle(oracle, tmp_path, dt):
+    """The d = 128 CTA-pair kernel (cta_group::2, one Q tile per CTA, two CTAs
+    per SM) is opt-in since the ping-pong kernel overtook it at long N
+    (FMHA_TUNE_PAIR128_N=8192, read once per process: a subprocess).  N = 8320
+    (an odd Q-tile count: the last pair has a padding CTA) plus an even case,
+    sampled Q tiles against the tile oracle."""
+    import os
+    import subprocess
+    import sys
+    cases = [(1, 8320, 2), (1, 8192, 3)]
+    probs = {}
+    for n, (L, N, h) in enumerate(cases):
+        q, k, v = oracle.problem(L, N, h, 128, 70 + n, dtype=dt)
+        probs[n] = (q, k, v)
+        np.savez(tmp_path / f"in{n}.npz", q=q, k=k, v=v)
+    code = (
+        "import numpy as np, torch, paper_2312_11918_b200 as fm\n"
+        f"td = torch.bfloat16 if {dt!r} == 'bf16' else torch.float16\n"
+        f"for n in range({len(cases)}):\n"
+        f"    z = np.load({str(tmp_path)!r} + f'/in{{n}}.npz')\n"
+        "    q, k, v = (torch.from_numpy(z[x]).cuda().to(td) for x in ('q', 'k', 'v'))\n"
+        "    L, N, h, d = q.shape\n"
+        "    assert 'pair_kernel<128,64>' in fm.kernel_for(L, N, h, d, fm.BF16 if td == torch.bfloat16 else fm.F16)\n"
+        "    o, lse = fm.fmha_fwd(q, k, v)\n"
+        f"    np.savez({str(tmp_path)!r} + f'/out{{n}}.npz', o=o.float().cpu().numpy(), lse=lse.cpu().numpy())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, FMHA_TUNE_PAIR128_N="8192"),
+                   cwd=root, timeout=600)
+    for n, (L, N, h) in enumerate(cases):
+        q, k, v = probs[n]
+        out = np.load(tmp_path / f"out{n}.npz")
+        tiles = [(0, hh, t) for hh in (0, h - 1) for t in (0, 31, (N - 1) // 128)]
+        o_ref, lse_ref = oracle.fmha_tiles(q, k, v, tiles, 128, 128)
+        for ti, (b, hh, t) in enumerate(tiles):
+            r0, r1 = t * 128, min(N, t * 128 + 128)
+            res = errors(out["o"][b, r0:r1, hh], out["lse"][b, hh, r0:r1], o_ref[ti][: r1 - r0],
+                         lse_ref[ti][: r1 - r0])
+            assert_within(res, f"pair128 {dt} N={N} h={h} tile {(b, hh, t)}")
 
 
 @pytest.mark.parametrize("env", ["FMHA_TUNE_DBS", "FMHA_TUNE_SPLIT"])

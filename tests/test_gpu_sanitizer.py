@@ -50,3 +50,20 @@ def test_memcheck_clean_double_buffered_s_kernel():
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+
+
+def test_memcheck_clean_d128_pair_kernel():
+    """The opt-in d = 128 CTA-pair kernel (FMHA_TUNE_PAIR128_N=8192) under memcheck."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    san = _sanitizer()
+    if san is None:
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "3", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_smoke.py"), "pair128"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, FMHA_TUNE_PAIR128_N="8192"))
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
