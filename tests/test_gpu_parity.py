@@ -308,12 +308,12 @@ def test_opt_in_d128_pair_kernel_against_oracle(oracle, tmp_path, dt):
     """The d = 128 CTA-pair kernel (cta_group::2, one Q tile per CTA, two CTAs
     per SM) is opt-in since the ping-pong kernel overtook it at long N
     (FMHA_TUNE_PAIR128_N=8192, read once per process: a subprocess).  N = 8320
-    (an odd Q-tile count: the last pair has a padding CTA) plus an even case,
+    (an odd Q-tile count per head: each head's last pair has a padding CTA) plus an even case,
     sampled Q tiles against the tile oracle."""
     import os
     import subprocess
     import sys
-    cases = [(1, 8320, 2), (1, 8192, 3)]
+    cases = [(1, 8320, 3), (1, 8192, 3)]  # > #SMs Q tiles: past the one-CTA-per-tile paths
     probs = {}
     for n, (L, N, h) in enumerate(cases):
         q, k, v = oracle.problem(L, N, h, 128, 70 + n, dtype=dt)
