@@ -453,7 +453,8 @@ cudaError_t copy_rows(char* dst, const char* src, const int64_t st[3], const fmh
 // ------------------------------------------------------- kernel choice --
 // Environment overrides for A/B tuning runs, read once per process:
 //   FMHA_TUNE_PAIR=0   no CTA-pair kernels;  FMHA_TUNE_D64=0  no two-CTA d=64
-//   kernel;  FMHA_TUNE_EMU / FMHA_TUNE_EMU64  exp2 split of the ping-pong kernel.
+//   kernel;  FMHA_TUNE_EMU / FMHA_TUNE_EMU64  exp2 split of the ping-pong kernel
+//   (d = 128 default: kEmuEdgeFree, the position-dependent FlashAttention-4 pattern).
 struct Tuning {
   bool pair_ok, d64_ok;
   int emu64, emu128;
@@ -472,7 +473,7 @@ const Tuning& tuning() {
       return e ? std::atoi(e) : dflt;
     };
     return Tuning{env("FMHA_TUNE_PAIR", 1) != 0, env("FMHA_TUNE_D64", 1) != 0, env("FMHA_TUNE_EMU64", -1),
-                  env("FMHA_TUNE_EMU", 4), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 1 << 30),
+                  env("FMHA_TUNE_EMU", fmha_b200::kEmuEdgeFree), env("FMHA_TUNE_SPLIT", 0), env("FMHA_TUNE_PAIR128_N", 1 << 30),
                   env("FMHA_TUNE_DBS", 0), env("FMHA_TUNE_EMU64D", 4),
                   env("FMHA_TUNE_D64_N", 1024), env("FMHA_TUNE_TINY", -1),
                   env("FMHA_TUNE_TINY2", -1)};
