@@ -140,7 +140,7 @@ __device__ __forceinline__ float exp_rowsum_pack(const float (&s)[kTotal], float
 #pragma unroll
   for (int i = 0; i < kCols / 2; ++i) {
     const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
-    const bool emu = kEmuPer16 == kEmuEdgeFree ? emulate_pair_at<kEmuPer16>(kOff / 2 + i) : emulate_pair<kEmuPer16>(i);
+    const bool emu = kEmuPer16 >= kEmuEdgeFree ? emulate_pair_at<kEmuPer16>(kOff / 2 + i) : emulate_pair<kEmuPer16>(i);
     const uint64_t e = emu ? exp2_poly_x2(x) : exp2_mufu_x2(x);
     if (i & 1)
       acc1 = fadd2(acc1, e);
@@ -166,7 +166,8 @@ __device__ __forceinline__ void exp_pack_inplace(float (&s)[kTotal], float c, fl
 #pragma unroll
   for (int i = 0; i < kCols / 2; ++i) {
     const uint64_t x = ffma2(f2_pack(s[kOff + 2 * i], s[kOff + 2 * i + 1]), c2, nm2);
-    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    const bool emu = kEmuPer16 >= kEmuEdgeFree ? emulate_pair_at<kEmuPer16>(kOff / 2 + i) : emulate_pair<kEmuPer16>(i);
+    const uint64_t e = emu ? exp2_poly_x2(x) : exp2_mufu_x2(x);
     f2_unpack(e, s[kOff + 2 * i], s[kOff + 2 * i + 1]);
     p[i] = pack2_x2<kBF16>(e);
   }
@@ -203,7 +204,8 @@ __device__ __forceinline__ float exp_rowsum_pack_max(const float (&s)[128], floa
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const uint64_t x = ffma2(f2_pack(s[2 * i], s[2 * i + 1]), c2, nm2);
-    const uint64_t e = emulate_pair<kEmuPer16>(i) ? exp2_poly_x2(x) : exp2_mufu_x2(x);
+    const bool emu = kEmuPer16 >= kEmuEdgeFree ? emulate_pair_at<kEmuPer16>(i) : emulate_pair<kEmuPer16>(i);
+    const uint64_t e = emu ? exp2_poly_x2(x) : exp2_mufu_x2(x);
     if (i & 1)
       acc1 = fadd2(acc1, e);
     else
