@@ -36,3 +36,24 @@ def test_kernel_choice_rejects_invalid_problems():
         fm.kernel_for(1, 0, 1, 64)
     with pytest.raises(ValueError):
         fm.kernel_for(1, 128, 1, 96)  # head dim without a kernel
+
+
+@pytest.mark.parametrize("env,shape,kernel", [
+    ({"FMHA_TUNE_PAIR128_N": "8192"}, (1, 8192, 3, 128), "fmha_fwd_pair_kernel<128,64>"),  # opt-in d=128 pairs
+    ({"FMHA_TUNE_PAIR128_N": "8192"}, (1, 4096, 8, 128), "fmha_fwd_sm100_kernel<128>"),    # below the cut
+    ({"FMHA_TUNE_PAIR": "0"}, (2, 8192, 8, 256), "fmha_fwd_st_kernel<256,128>"),          # no CTA pairs at all
+    ({"FMHA_TUNE_DBS": "1"}, (4, 4096, 16, 128), "fmha_fwd_dbs_kernel<128>"),
+    ({"FMHA_TUNE_TINY": "0", "FMHA_TUNE_TINY2": "0"}, (1, 512, 1, 64), "fmha_fwd_sm100_kernel<64>"),
+    ({"FMHA_TUNE_D64": "0"}, (16, 512, 12, 64), "fmha_fwd_sm100_kernel<64>"),
+])
+def test_kernel_choice_overrides(env, shape, kernel):
+    """The FMHA_TUNE_* overrides (read once per process, so each case runs in a
+    subprocess; host-only, no CUDA call)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"import paper_2312_11918_b200 as fm; print(fm.kernel_for(*{shape!r}))"
+    out = subprocess.run([sys.executable, "-c", code], check=True, cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, **env), timeout=120).stdout
+    assert out.startswith(kernel), out
